@@ -1,0 +1,126 @@
+/* polyjac_b200 — C ABI of the B200-native evaluator for sparse polynomial systems and their
+ * full Jacobians (arXiv 1201.0499), complex double and complex double-double.
+ *
+ * This is the drop-in boundary for the reference's hot path (ref = /root/reference/proj).
+ * Each entry point names the reference interface it replaces. Plain pointers and sizes
+ * only; no C++ or torch types. Errors are status codes; pj_last_error() returns the
+ * calling thread's last message (the reference throws instead: the C++ wrapper
+ * include/polyjac_b200.hpp maps the codes back onto the same exception types).
+ *
+ * Array conventions
+ *   positions, exponents  int32 [n*m*k], S_m order: monomial s = p*m + g, slot s*k + j
+ *                         (ref include/polyjac/system.hpp:28-31, packing.hpp:12-15);
+ *                         positions 0-based and strictly increasing, exponents in [1, d]
+ *   coeffs                double [n*m][4] = (re_hi, re_lo, im_hi, im_lo); lo words may be 0
+ *                         (double input). PJ_PREC_D uses the hi words only.
+ *   points                double [batch][n][W]
+ *   out                   double [batch][n + n*n][W]: the n values, then the row-major
+ *                         Jacobian, entry (p, i) at n + p*n + i (ref system.hpp:48-54)
+ *   W = 2 (re, im) for PJ_PREC_D, 4 (re_hi, re_lo, im_hi, im_lo) for PJ_PREC_DD.
+ */
+#ifndef POLYJAC_B200_H
+#define POLYJAC_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* status codes */
+#define PJ_OK 0
+#define PJ_EINVAL 1     /* std::invalid_argument in the reference */
+#define PJ_ERANGE 2     /* std::out_of_range in the reference */
+#define PJ_ECUDA 3      /* CUDA runtime failure (message in pj_last_error) */
+#define PJ_ENOMEM 4     /* device allocation failed */
+#define PJ_ENONFINITE 5 /* non-finite coordinate: std::invalid_argument in
+                           ref src/engine.cpp:186-188 */
+
+/* precision / order flags for pj_evaluate */
+#define PJ_PREC_D 1         /* complex double, reference operation order: bit-exact with
+                               EvaluationContext::evaluate (ref src/engine.cpp:181-224) */
+#define PJ_PREC_DD 2        /* complex double-double */
+#define PJ_ORDER_REF 0x10   /* dd: keep the reference order in every stage (bit-exact with the
+                               oracle's dd restatement); default dd order is the fast one */
+#define PJ_ORDER_FAST 0x20  /* d: allow the fast order (default for d is the reference order) */
+
+typedef struct pj_system_desc {
+    int32_t n, m, k, d;
+    const int32_t* positions;
+    const int32_t* exponents;
+    const double* coeffs;
+} pj_system_desc;
+
+typedef struct pj_ctx pj_ctx;
+
+/* Thread-local message of the last failing call ("" after success). */
+const char* pj_last_error(void);
+
+/* Library / build identification string. */
+const char* pj_version(void);
+
+/* Number of rule violations of the system (0 = valid); the first one's text is copied into
+ * msg (capacity cap, may be NULL). Replaces validate_system, ref src/system.cpp:21-64. */
+int pj_validate(const pj_system_desc* sys, char* msg, size_t cap);
+
+/* Context creation: validate + pack + upload once; replaces
+ * EvaluationContext::EvaluationContext(sys, GridConfig), ref src/engine.cpp:168-179 and
+ * build_layout, ref src/packing.cpp:19-52 (PJ_EINVAL for an invalid system or n > 256). */
+int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out);
+void pj_ctx_destroy(pj_ctx* ctx);
+
+/* Evaluate `batch` points already resident on the context's device; asynchronous on
+ * `stream` (a cudaStream_t, NULL = legacy default stream). Replaces
+ * EvaluationContext::evaluate / evaluate_batch, ref src/engine.cpp:181-260, batched over
+ * points. The caller owns both buffers; no allocation happens here. batch == 0 is a no-op.
+ * Non-finite coordinates are flagged on device: read with pj_nonfinite_seen. */
+int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, double* d_out, void* stream);
+
+/* Host-buffer convenience: H2D of the points, pj_evaluate, D2H of the results, synchronous.
+ * Returns PJ_ENONFINITE (like the reference's throw) when an input coordinate is non-finite. */
+int pj_evaluate_host(pj_ctx* ctx, int flags, const double* h_points, int64_t batch, double* h_out);
+
+/* Synchronises `stream`, then reports (and clears) whether any pj_evaluate since the last
+ * call saw a non-finite coordinate. */
+int pj_nonfinite_seen(pj_ctx* ctx, void* stream, int* seen);
+
+/* Shape of the packed layout: n, m, k, d, and the reference's constant-memory-equivalent
+ * footprint 2*n*m*k (PackedLayout::footprint_bytes, ref include/polyjac/packing.hpp:44-45). */
+int pj_layout_info(const pj_ctx* ctx, int32_t* n, int32_t* m, int32_t* k, int32_t* d, int64_t* footprint_bytes);
+
+/* Index maps, bit-exact with the reference:
+ *   pj_mons_slot      mons_slot, ref src/packing.cpp:8-17 (kind 0 = value, 1 = derivative;
+ *                     PJ_ERANGE where the reference throws std::out_of_range)
+ *   pj_slot_targets   stage2_slot_targets, ref src/kernels.cpp:129-137 (k+1 slots, value last)
+ *   pj_zero_mask      zero_mask, ref src/packing.cpp:54-72, regenerated as the complement of
+ *                     the device gather map; returns its length (needs cap >= length) */
+int pj_mons_slot(int64_t s, int kind, int var, int n, int m, int64_t* slot);
+int pj_slot_targets(const pj_ctx* ctx, int64_t s, int64_t* targets);
+int64_t pj_zero_mask(const pj_ctx* ctx, int64_t* mask, int64_t cap);
+
+/* Multiplication tally of `evals` evaluations (MultCounter, ref include/polyjac/kernels.hpp:15-34;
+ * closed form SPEC.md:477): counts[5] = stage1_powers, stage1_factors, stage2, speelpenning, stage3. */
+int pj_mult_counts(const pj_ctx* ctx, int64_t evals, uint64_t* counts);
+
+/* Deterministic inputs, bit-identical to random_system / random_points
+ * (ref src/system.cpp:66-118, ref src/rng.hpp): coeffs get lo words 0; points are [count][n][2]. */
+int pj_random_system(int n, int m, int k, int d, uint64_t seed, int32_t* positions, int32_t* exponents,
+                     double* coeffs);
+int pj_random_points(int n, int64_t count, uint64_t seed, double* points);
+
+/* Advanced: override the launch shape for `flags`' precision (threads per CTA, multiple of 32,
+ * <= 256; points per CTA tile). 0 restores the automatic choice. */
+int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points);
+/* Report the launch shape used for `flags`: threads, tile points, blocks, dynamic smem bytes. */
+int pj_get_launch(pj_ctx* ctx, int flags, int32_t* threads, int32_t* tile_points, int32_t* blocks,
+                  int64_t* smem_bytes);
+
+/* Measurement helper (not part of the reference surface): FP64 DFMA throughput of `device`
+ * in TFLOP/s (2 flops per DFMA), the denominator of the roofline fraction. */
+int pj_fp64_peak_probe(int device, double* tflops);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POLYJAC_B200_H */

@@ -1,0 +1,642 @@
+// Host side of the C ABI (include/polyjac_b200.h): validation, packing v2, the stage-3 gather
+// map, device residency, launch shape, and the deterministic input generator.
+//
+// Compiled with -ffp-contract=off: the double-double power-rule pre-scale below must round
+// exactly like the oracle's restatement.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "../../include/polyjac_b200.h"
+#include "eval_kernels.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+int cuda_fail(cudaError_t e, const char* what) {
+    g_err = std::string(what) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? PJ_ENOMEM : PJ_ECUDA;
+}
+#define PJ_CUDA(call)                                      \
+    do {                                                   \
+        cudaError_t e_ = (call);                           \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+// ------------------------------------------------------------------ validation
+// Rules and wording follow validate_system, ref src/system.cpp:21-64 (violations as data);
+// the byte-encoding cap n <= 256 follows build_layout, ref src/packing.cpp:25-27.
+struct Violation {
+    int poly, mono;
+    std::string rule;
+    std::string describe() const {
+        if (poly >= 0 && mono >= 0)
+            return "polynomial " + std::to_string(poly) + ", monomial " + std::to_string(mono) + ": " + rule;
+        if (poly >= 0) return "polynomial " + std::to_string(poly) + ": " + rule;
+        return rule;
+    }
+};
+
+std::vector<Violation> validate(const pj_system_desc& S) {
+    std::vector<Violation> v;
+    auto flag = [&](int p, int g, const char* r) { v.push_back({p, g, r}); };
+    if (S.n < 1) flag(-1, -1, "n must be at least 1");
+    if (S.m < 1) flag(-1, -1, "m must be at least 1");
+    if (S.k < 1) flag(-1, -1, "k must be at least 1");
+    if (S.k > S.n) flag(-1, -1, "k exceeds n");
+    if (S.d < 1) flag(-1, -1, "d must be at least 1");
+    if (S.d > 255) flag(-1, -1, "d exceeds 255");
+    if (!v.empty() && (S.n < 1 || S.m < 1 || S.k < 1)) return v;  // per-term checks need a shape
+    if (!S.positions || !S.exponents || !S.coeffs) {
+        flag(-1, -1, "term count is not n*m");
+        return v;
+    }
+    for (int p = 0; p < S.n; ++p)
+        for (int g = 0; g < S.m; ++g) {
+            const size_t s = size_t(p) * S.m + g;
+            const double re = S.coeffs[4 * s], im = S.coeffs[4 * s + 2];
+            const double rl = S.coeffs[4 * s + 1], il = S.coeffs[4 * s + 3];
+            if (!std::isfinite(re) || !std::isfinite(im) || !std::isfinite(rl) || !std::isfinite(il))
+                flag(p, g, "non-finite coefficient");
+            if (re == 0.0 && im == 0.0 && rl == 0.0 && il == 0.0) flag(p, g, "zero coefficient");
+            for (int j = 0; j < S.k; ++j) {
+                const int pos = S.positions[s * S.k + j], e = S.exponents[s * S.k + j];
+                if (pos < 0 || pos >= S.n) flag(p, g, "variable index out of range [0,n-1]");
+                if (j > 0 && pos <= S.positions[s * S.k + j - 1]) flag(p, g, "positions not strictly increasing");
+                if (e < 1 || e > S.d) flag(p, g, "exponent out of range [1,d]");
+            }
+        }
+    return v;
+}
+
+// ------------------------------------------------------------------ dd pre-scale (host)
+// a * (hi, lo) for a small integer a: TwoProd of the high word via FMA, the low word folded
+// in, one Fast2Sum. Exact for a <= 255 and a double coefficient.
+void dd_mul_small(double hi, double lo, double a, double* oh, double* ol) {
+    double p = hi * a;
+    double e = std::fma(hi, a, -p);
+    e = std::fma(lo, a, e);
+    double s = p + e;
+    *oh = s;
+    *ol = e - (s - p);
+}
+
+struct PrecState {
+    double* coef = nullptr;   // device planes
+    pjb::LaunchCfg cfg;       // automatic or overridden
+    int over_threads = 0, over_tp = 0;
+    bool cfg_ready = false;
+};
+
+}  // namespace
+
+struct pj_ctx {
+    int device = 0;
+    int sms = 0;
+    size_t smem_optin = 0;
+    int n, m, k, d, kp, chunks;
+    std::vector<int32_t> pos, exps;  // host copies (index maps)
+    std::vector<int> gm_off;
+    std::vector<uint16_t> gm_ent;
+    uint16_t* d_posexp = nullptr;
+    int* d_gm_off = nullptr;
+    uint16_t* d_gm_ent = nullptr;
+    int* d_flag = nullptr;
+    PrecState prec[2];  // [0] = d, [1] = dd
+    double* d_scratch = nullptr;
+    size_t scratch_bytes = 0;
+    // host-API staging buffers
+    double* d_in = nullptr;
+    double* d_out = nullptr;
+    size_t in_cap = 0, out_cap = 0;
+    cudaStream_t hstream = nullptr;
+
+    pjb::DevSystem dev(int pi) const {
+        pjb::DevSystem S;
+        S.n = n;
+        S.m = m;
+        S.k = k;
+        S.d = d;
+        S.nm = n * m;
+        S.chunks = chunks;
+        S.kp = kp;
+        S.posexp = d_posexp;
+        S.coef = prec[pi].coef;
+        S.gm_off = d_gm_off;
+        S.gm_ent = d_gm_ent;
+        return S;
+    }
+};
+
+namespace {
+
+void free_ctx(pj_ctx* c) {
+    if (!c) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(c->device);
+    cudaFree(c->d_posexp);
+    cudaFree(c->d_gm_off);
+    cudaFree(c->d_gm_ent);
+    cudaFree(c->d_flag);
+    cudaFree(c->prec[0].coef);
+    cudaFree(c->prec[1].coef);
+    cudaFree(c->d_scratch);
+    cudaFree(c->d_in);
+    cudaFree(c->d_out);
+    if (c->hstream) cudaStreamDestroy(c->hstream);
+    cudaSetDevice(prev);
+    delete c;
+}
+
+// Shared-memory footprint of one CTA: TP points' power tables + per-warp staging and
+// accumulators (see eval_kernels.cu).
+size_t smem_need(const pj_ctx* c, int W, int nw, int tp) {
+    const size_t D1 = c->d > 2 ? c->d - 1 : 1;
+    const size_t tab = D1 * W * c->n;
+    const size_t per_warp = size_t(c->k + 1) * W * 32 + size_t(c->n + 1) * W;
+    return (tp * tab + nw * per_warp) * sizeof(double);
+}
+
+int choose_launch(pj_ctx* c, int pi) {
+    PrecState& P = c->prec[pi];
+    const int W = pi == 0 ? 2 : 4;
+    const int precflag = pi == 0 ? 1 : 2;
+    int best_score = -1;
+    pjb::LaunchCfg best;
+    std::vector<int> nws = {8, 4, 2, 1}, tps = {8, 4, 2, 1};
+    if (P.over_threads) nws = {P.over_threads / 32};
+    if (P.over_tp) tps = {P.over_tp};
+    for (int nw : nws) {
+        for (int tp : tps) {
+            const size_t sm = smem_need(c, W, nw, tp);
+            if (sm > c->smem_optin) continue;
+            const int nb = pjb::max_blocks_per_sm(precflag, 0, nw * 32, sm);
+            if (nb <= 0) continue;
+            // resident warps first; then fewer, fatter tiles (more coefficient reuse) as long as
+            // a tile still has a task per warp
+            const int warps = std::min(nb * nw, 64);
+            const int score = warps * 64 + (tp * c->n >= nw ? tp : 0);
+            if (score > best_score) {
+                best_score = score;
+                best.threads = nw * 32;
+                best.tp = tp;
+                best.smem_bytes = sm;
+                best.blocks = nb * c->sms;
+            }
+        }
+    }
+    if (best_score < 0) {
+        // global-scratch fallback for systems whose tables exceed shared memory
+        const int nw = P.over_threads ? P.over_threads / 32 : 4;
+        const int tp = P.over_tp ? P.over_tp : 1;
+        best.threads = nw * 32;
+        best.tp = tp;
+        best.smem_bytes = 0;
+        best.blocks = c->sms * 4;
+        const size_t need = smem_need(c, W, nw, tp) * best.blocks;
+        if (need > c->scratch_bytes) {
+            cudaFree(c->d_scratch);
+            c->d_scratch = nullptr;
+            c->scratch_bytes = 0;
+            PJ_CUDA(cudaMalloc(&c->d_scratch, need));
+            c->scratch_bytes = need;
+        }
+        best.gscratch = c->d_scratch;
+    }
+    best.flag = c->d_flag;
+    P.cfg = best;
+    P.cfg_ready = true;
+    return PJ_OK;
+}
+
+int check_desc(const pj_system_desc* sys) {
+    if (!sys) return fail(PJ_EINVAL, "null system descriptor");
+    auto v = validate(*sys);
+    if (!v.empty()) return fail(PJ_EINVAL, "build_layout: invalid system: " + v.front().describe());
+    if (sys->n > 256) return fail(PJ_EINVAL, "build_layout: n > 256 does not fit the byte encoding");
+    return PJ_OK;
+}
+
+}  // namespace
+
+extern "C" {
+#pragma GCC visibility push(default)
+
+const char* pj_last_error(void) { return g_err.c_str(); }
+
+const char* pj_version(void) { return "polyjac_b200 0.1 (sm_100a)"; }
+
+int pj_validate(const pj_system_desc* sys, char* msg, size_t cap) {
+    if (!sys) return fail(-1, "null system descriptor");
+    auto v = validate(*sys);
+    if (msg && cap) {
+        std::string s = v.empty() ? "" : v.front().describe();
+        std::strncpy(msg, s.c_str(), cap - 1);
+        msg[cap - 1] = 0;
+    }
+    g_err.clear();
+    return int(v.size());
+}
+
+int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
+    if (!out) return fail(PJ_EINVAL, "null output pointer");
+    *out = nullptr;
+    int rc = check_desc(sys);
+    if (rc) return rc;
+    pj_ctx* c = new pj_ctx();
+    c->device = device;
+    c->n = sys->n;
+    c->m = sys->m;
+    c->k = sys->k;
+    c->d = sys->d;
+    c->kp = (sys->k + 7) / 8 * 8;
+    c->chunks = (sys->m + 31) / 32;
+    const size_t nm = size_t(c->n) * c->m, k = c->k;
+    c->pos.assign(sys->positions, sys->positions + nm * k);
+    c->exps.assign(sys->exponents, sys->exponents + nm * k);
+
+    // packing v2: fused position/exponent words (ref src/packing.cpp:40-44)
+    std::vector<uint16_t> posexp(nm * c->kp, 0);
+    for (size_t s = 0; s < nm; ++s)
+        for (size_t j = 0; j < k; ++j)
+            posexp[s * c->kp + j] = uint16_t(c->pos[s * k + j] | ((c->exps[s * k + j] - 1) << 8));
+    // coefficient planes, derivative-major with the power rule folded in (ref src/packing.cpp:46-49):
+    // double: a*c rounded per component, exactly as the reference; dd: exact.
+    std::vector<double> cd((k + 1) * 2 * nm), cdd((k + 1) * 4 * nm);
+    for (size_t s = 0; s < nm; ++s) {
+        const double* C = sys->coeffs + 4 * s;
+        for (size_t j = 0; j <= k; ++j) {
+            const double a = j < k ? double(c->exps[s * k + j]) : 1.0;
+            if (j < k) {
+                cd[(j * 2 + 0) * nm + s] = a * C[0];
+                cd[(j * 2 + 1) * nm + s] = a * C[2];
+                double h, l;
+                dd_mul_small(C[0], C[1], a, &h, &l);
+                cdd[(j * 4 + 0) * nm + s] = h;
+                cdd[(j * 4 + 1) * nm + s] = l;
+                dd_mul_small(C[2], C[3], a, &h, &l);
+                cdd[(j * 4 + 2) * nm + s] = h;
+                cdd[(j * 4 + 3) * nm + s] = l;
+            } else {
+                cd[(j * 2 + 0) * nm + s] = C[0];
+                cd[(j * 2 + 1) * nm + s] = C[2];
+                for (int q = 0; q < 4; ++q) cdd[(j * 4 + q) * nm + s] = C[q];
+            }
+        }
+    }
+    // stage-3 gather map: for (row p, chunk c, column v) the ascending-g list of (g, j) with
+    // positions[s*k+j] == v — the inverse of the reference's derivative slot map
+    // mons_slot(s, derivative, v) = g*(n^2+n) + (v+1)*n + p (ref src/packing.cpp:8-17)
+    const int n = c->n, C = c->chunks;
+    std::vector<int> cnt(size_t(n) * C * n + 1, 0);
+    for (int p = 0; p < n; ++p)
+        for (int g = 0; g < c->m; ++g)
+            for (size_t j = 0; j < k; ++j) {
+                const size_t s = size_t(p) * c->m + g;
+                cnt[(size_t(p) * C + g / 32) * n + c->pos[s * k + j]]++;
+            }
+    c->gm_off.assign(cnt.size(), 0);
+    for (size_t i = 0; i + 1 < cnt.size(); ++i) c->gm_off[i + 1] = c->gm_off[i] + cnt[i];
+    c->gm_ent.assign(c->gm_off.back(), 0);
+    {
+        std::vector<int> fill(c->gm_off.begin(), c->gm_off.end() - 1);
+        for (int p = 0; p < n; ++p)
+            for (int g = 0; g < c->m; ++g)  // ascending g: lists come out sorted
+                for (size_t j = 0; j < k; ++j) {
+                    const size_t s = size_t(p) * c->m + g;
+                    const size_t li = (size_t(p) * C + g / 32) * n + c->pos[s * k + j];
+                    c->gm_ent[fill[li]++] = uint16_t(j * 32 + (g & 31));
+                }
+    }
+
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        free_ctx(c);
+        return cuda_fail(e, "cudaSetDevice");
+    }
+    auto up = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
+        cudaError_t r = cudaMalloc(dst, bytes ? bytes : 16);
+        if (r) return r;
+        return bytes ? cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+    };
+    cudaDeviceProp prop;
+    if ((e = cudaGetDeviceProperties(&prop, device)) ||
+        (e = up((void**)&c->d_posexp, posexp.data(), posexp.size() * 2)) ||
+        (e = up((void**)&c->prec[0].coef, cd.data(), cd.size() * 8)) ||
+        (e = up((void**)&c->prec[1].coef, cdd.data(), cdd.size() * 8)) ||
+        (e = up((void**)&c->d_gm_off, c->gm_off.data(), c->gm_off.size() * 4)) ||
+        (e = up((void**)&c->d_gm_ent, c->gm_ent.data(), c->gm_ent.size() * 2)) ||
+        (e = cudaMalloc((void**)&c->d_flag, sizeof(int))) || (e = cudaMemset(c->d_flag, 0, sizeof(int))) ||
+        (e = cudaStreamCreateWithFlags(&c->hstream, cudaStreamNonBlocking))) {
+        free_ctx(c);
+        cudaSetDevice(prev);
+        return cuda_fail(e, "pj_ctx_create: device upload");
+    }
+    c->sms = prop.multiProcessorCount;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
+    e = pjb::set_smem_attr(c->smem_optin);
+    if (e) {
+        free_ctx(c);
+        cudaSetDevice(prev);
+        return cuda_fail(e, "pj_ctx_create: smem attribute");
+    }
+    for (int pi = 0; pi < 2; ++pi) {
+        rc = choose_launch(c, pi);
+        if (rc) {
+            free_ctx(c);
+            cudaSetDevice(prev);
+            return rc;
+        }
+    }
+    cudaSetDevice(prev);
+    g_err.clear();
+    *out = c;
+    return PJ_OK;
+}
+
+void pj_ctx_destroy(pj_ctx* ctx) { free_ctx(ctx); }
+
+static int prec_index(int flags) {
+    const int p = flags & 0x0f;
+    return p == PJ_PREC_D ? 0 : p == PJ_PREC_DD ? 1 : -1;
+}
+static int order_of(int flags) {
+    if ((flags & 0x0f) == PJ_PREC_D) return (flags & PJ_ORDER_FAST) ? 1 : 0;
+    return (flags & PJ_ORDER_REF) ? 0 : 1;
+}
+
+int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, double* d_out, void* stream) {
+    if (!ctx) return fail(PJ_EINVAL, "null context");
+    const int pi = prec_index(flags);
+    if (pi < 0) return fail(PJ_EINVAL, "evaluate: unknown precision flag");
+    if (batch < 0) return fail(PJ_EINVAL, "evaluate: negative batch");
+    if (batch == 0) {
+        g_err.clear();
+        return PJ_OK;
+    }
+    if (!d_points || !d_out) return fail(PJ_EINVAL, "evaluate: null buffer");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != ctx->device) PJ_CUDA(cudaSetDevice(ctx->device));
+    cudaError_t e = pjb::launch_eval(pi + 1, order_of(flags), ctx->prec[pi].cfg, ctx->dev(pi), d_points, d_out,
+                                     (long long)batch, (cudaStream_t)stream);
+    if (prev != ctx->device) cudaSetDevice(prev);
+    if (e) return cuda_fail(e, "evaluate: kernel launch");
+    g_err.clear();
+    return PJ_OK;
+}
+
+int pj_nonfinite_seen(pj_ctx* ctx, void* stream, int* seen) {
+    if (!ctx || !seen) return fail(PJ_EINVAL, "null argument");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != ctx->device) PJ_CUDA(cudaSetDevice(ctx->device));
+    int h = 0;
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(&h, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream)) ||
+        (e = cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), (cudaStream_t)stream)) ||
+        (e = cudaStreamSynchronize((cudaStream_t)stream))) {
+        if (prev != ctx->device) cudaSetDevice(prev);
+        return cuda_fail(e, "pj_nonfinite_seen");
+    }
+    if (prev != ctx->device) cudaSetDevice(prev);
+    *seen = h;
+    g_err.clear();
+    return PJ_OK;
+}
+
+int pj_evaluate_host(pj_ctx* ctx, int flags, const double* h_points, int64_t batch, double* h_out) {
+    if (!ctx) return fail(PJ_EINVAL, "null context");
+    const int pi = prec_index(flags);
+    if (pi < 0) return fail(PJ_EINVAL, "evaluate: unknown precision flag");
+    if (batch < 0) return fail(PJ_EINVAL, "evaluate: negative batch");
+    if (batch == 0) {
+        g_err.clear();
+        return PJ_OK;
+    }
+    if (!h_points || !h_out) return fail(PJ_EINVAL, "evaluate: null buffer");
+    const int W = pi == 0 ? 2 : 4;
+    const size_t in_b = size_t(batch) * ctx->n * W * 8;
+    const size_t out_b = size_t(batch) * (size_t(ctx->n) * ctx->n + ctx->n) * W * 8;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    PJ_CUDA(cudaSetDevice(ctx->device));
+    if (in_b > ctx->in_cap) {
+        cudaFree(ctx->d_in);
+        ctx->d_in = nullptr;
+        ctx->in_cap = 0;
+        PJ_CUDA(cudaMalloc(&ctx->d_in, in_b));
+        ctx->in_cap = in_b;
+    }
+    if (out_b > ctx->out_cap) {
+        cudaFree(ctx->d_out);
+        ctx->d_out = nullptr;
+        ctx->out_cap = 0;
+        PJ_CUDA(cudaMalloc(&ctx->d_out, out_b));
+        ctx->out_cap = out_b;
+    }
+    cudaStream_t st = ctx->hstream;
+    PJ_CUDA(cudaMemcpyAsync(ctx->d_in, h_points, in_b, cudaMemcpyHostToDevice, st));
+    int rc = pj_evaluate(ctx, flags, ctx->d_in, batch, ctx->d_out, st);
+    if (rc) {
+        cudaSetDevice(prev);
+        return rc;
+    }
+    PJ_CUDA(cudaMemcpyAsync(h_out, ctx->d_out, out_b, cudaMemcpyDeviceToHost, st));
+    int seen = 0;
+    rc = pj_nonfinite_seen(ctx, st, &seen);
+    cudaSetDevice(prev);
+    if (rc) return rc;
+    if (seen) return fail(PJ_ENONFINITE, "evaluate: non-finite coordinate");
+    g_err.clear();
+    return PJ_OK;
+}
+
+int pj_layout_info(const pj_ctx* ctx, int32_t* n, int32_t* m, int32_t* k, int32_t* d, int64_t* footprint) {
+    if (!ctx) return fail(PJ_EINVAL, "null context");
+    if (n) *n = ctx->n;
+    if (m) *m = ctx->m;
+    if (k) *k = ctx->k;
+    if (d) *d = ctx->d;
+    if (footprint) *footprint = 2 * int64_t(ctx->n) * ctx->m * ctx->k;
+    g_err.clear();
+    return PJ_OK;
+}
+
+int pj_mons_slot(int64_t s, int kind, int var, int n, int m, int64_t* slot) {
+    const int64_t nm = int64_t(n) * m;
+    if (s < 0 || s >= nm) return fail(PJ_ERANGE, "mons_slot: monomial index " + std::to_string(s));
+    const int64_t p = s / m, g = s % m, stride = int64_t(n) * n + n;
+    if (kind == 0) {
+        *slot = g * stride + p;
+    } else {
+        if (var < 0 || var >= n) return fail(PJ_ERANGE, "mons_slot: variable " + std::to_string(var));
+        *slot = g * stride + int64_t(var + 1) * n + p;
+    }
+    g_err.clear();
+    return PJ_OK;
+}
+
+int pj_slot_targets(const pj_ctx* ctx, int64_t s, int64_t* targets) {
+    if (!ctx) return fail(PJ_EINVAL, "null context");
+    for (int j = 0; j < ctx->k; ++j) {
+        int rc = pj_mons_slot(s, 1, s >= 0 && s < int64_t(ctx->n) * ctx->m ? ctx->pos[s * ctx->k + j] : 0,
+                              ctx->n, ctx->m, targets + j);
+        if (rc) return rc;
+    }
+    return pj_mons_slot(s, 0, -1, ctx->n, ctx->m, targets + ctx->k);
+}
+
+int64_t pj_zero_mask(const pj_ctx* ctx, int64_t* mask, int64_t cap) {
+    if (!ctx) return fail(-1, "null context");
+    // Regenerated from the device gather map: a Mons slot is claimed iff it is a value slot or
+    // its (p, v, g) appears in the (p, chunk(g), v) list. Everything else is the zero mask.
+    const int64_t n = ctx->n, m = ctx->m, C = ctx->chunks, stride = n * n + n;
+    std::vector<unsigned char> claimed(size_t(stride * m), 0);
+    for (int64_t p = 0; p < n; ++p)
+        for (int64_t g = 0; g < m; ++g) claimed[size_t(g * stride + p)] = 1;
+    for (int64_t p = 0; p < n; ++p)
+        for (int64_t c = 0; c < C; ++c)
+            for (int64_t v = 0; v < n; ++v) {
+                const size_t li = size_t((p * C + c) * n + v);
+                for (int e = ctx->gm_off[li]; e < ctx->gm_off[li + 1]; ++e) {
+                    const int64_t g = c * 32 + (ctx->gm_ent[e] & 31);
+                    claimed[size_t(g * stride + (v + 1) * n + p)] = 1;
+                }
+            }
+    int64_t len = 0;
+    for (int64_t i = 0; i < stride * m; ++i)
+        if (!claimed[size_t(i)]) {
+            if (len < cap && mask) mask[len] = i;
+            ++len;
+        }
+    g_err.clear();
+    return len;
+}
+
+int pj_mult_counts(const pj_ctx* ctx, int64_t evals, uint64_t* counts) {
+    if (!ctx || !counts) return fail(PJ_EINVAL, "null argument");
+    const uint64_t n = ctx->n, nm = uint64_t(ctx->n) * ctx->m, k = ctx->k, d = ctx->d;
+    const uint64_t sp = k >= 3 ? 3 * k - 6 : 0;
+    counts[0] = uint64_t(evals) * n * (d >= 2 ? d - 2 : 0);
+    counts[1] = uint64_t(evals) * nm * (k - 1);
+    counts[2] = uint64_t(evals) * nm * (sp + 2 * k + 2);
+    counts[3] = uint64_t(evals) * nm * sp;
+    counts[4] = 0;
+    g_err.clear();
+    return PJ_OK;
+}
+
+// ------------------------------------------------------------------ input generator
+// Same published algorithm as ref src/system.cpp:66-118 and src/rng.hpp: std::mt19937_64
+// (output pinned by the standard), Lemire's multiply-shift bounded draw with rejection, and a
+// 53-bit uniform mapped to [-1, 1). Monomial supports: partial Fisher-Yates k-subset, sorted;
+// exponents 1 + below(d); coefficient components redrawn while both are zero.
+namespace {
+struct Gen {
+    std::mt19937_64 e;
+    explicit Gen(uint64_t seed) : e(seed) {}
+    uint64_t below(uint64_t bound) {
+        uint64_t x = e();
+        __uint128_t mm = (__uint128_t)x * bound;
+        uint64_t lo = uint64_t(mm);
+        if (lo < bound) {
+            const uint64_t thr = (0 - bound) % bound;
+            while (lo < thr) {
+                x = e();
+                mm = (__uint128_t)x * bound;
+                lo = uint64_t(mm);
+            }
+        }
+        return uint64_t(mm >> 64);
+    }
+    double sym() { return 2.0 * (double(e() >> 11) * 0x1p-53) - 1.0; }
+};
+}  // namespace
+
+int pj_random_system(int n, int m, int k, int d, uint64_t seed, int32_t* positions, int32_t* exponents,
+                     double* coeffs) {
+    if (n < 1) return fail(PJ_EINVAL, "random_system: n must be at least 1");
+    if (m < 1) return fail(PJ_EINVAL, "random_system: m must be at least 1");
+    if (k < 1 || k > n) return fail(PJ_EINVAL, "random_system: need 1 <= k <= n");
+    if (d < 1 || d > 255) return fail(PJ_EINVAL, "random_system: need 1 <= d <= 255");
+    Gen r(seed);
+    std::vector<int> idx(n);
+    for (size_t s = 0; s < size_t(n) * m; ++s) {
+        for (int i = 0; i < n; ++i) idx[i] = i;
+        for (int j = 0; j < k; ++j) std::swap(idx[j], idx[j + int(r.below(uint64_t(n - j)))]);
+        std::sort(idx.begin(), idx.begin() + k);
+        for (int j = 0; j < k; ++j) positions[s * k + j] = idx[j];
+        for (int j = 0; j < k; ++j) exponents[s * k + j] = 1 + int(r.below(uint64_t(d)));
+        double re, im;
+        do {
+            re = r.sym();
+            im = r.sym();
+        } while (re == 0.0 && im == 0.0);
+        coeffs[4 * s + 0] = re;
+        coeffs[4 * s + 1] = 0.0;
+        coeffs[4 * s + 2] = im;
+        coeffs[4 * s + 3] = 0.0;
+    }
+    g_err.clear();
+    return PJ_OK;
+}
+
+int pj_random_points(int n, int64_t count, uint64_t seed, double* points) {
+    if (n < 1 || count < 0) return fail(PJ_EINVAL, "random_points: bad shape");
+    Gen r(seed);
+    for (int64_t i = 0; i < count * n; ++i) {
+        points[2 * i] = r.sym();
+        points[2 * i + 1] = r.sym();
+    }
+    g_err.clear();
+    return PJ_OK;
+}
+
+int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points) {
+    if (!ctx) return fail(PJ_EINVAL, "null context");
+    const int pi = prec_index(flags);
+    if (pi < 0) return fail(PJ_EINVAL, "unknown precision flag");
+    if (threads < 0 || threads > 256 || threads % 32) return fail(PJ_EINVAL, "threads must be a multiple of 32 <= 256");
+    if (tile_points < 0) return fail(PJ_EINVAL, "tile_points must be >= 0");
+    ctx->prec[pi].over_threads = threads;
+    ctx->prec[pi].over_tp = tile_points;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(ctx->device);
+    int rc = choose_launch(ctx, pi);
+    cudaSetDevice(prev);
+    if (!rc) g_err.clear();
+    return rc;
+}
+
+int pj_get_launch(pj_ctx* ctx, int flags, int32_t* threads, int32_t* tile_points, int32_t* blocks,
+                  int64_t* smem_bytes) {
+    if (!ctx) return fail(PJ_EINVAL, "null context");
+    const int pi = prec_index(flags);
+    if (pi < 0) return fail(PJ_EINVAL, "unknown precision flag");
+    const pjb::LaunchCfg& L = ctx->prec[pi].cfg;
+    if (threads) *threads = L.threads;
+    if (tile_points) *tile_points = L.tp;
+    if (blocks) *blocks = L.blocks;
+    if (smem_bytes) *smem_bytes = int64_t(L.smem_bytes);
+    g_err.clear();
+    return PJ_OK;
+}
+
+#pragma GCC visibility pop
+}  // extern "C"

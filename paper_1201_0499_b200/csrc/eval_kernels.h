@@ -1,0 +1,43 @@
+// Device-side system layout ("packing v2") and launch plumbing shared by capi.cpp and
+// eval_kernels.cu. Built once per context on the host (capi.cpp: pack_system), uploaded once,
+// reused for every batch.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace pjb {
+
+struct DevSystem {
+    int n, m, k, d, nm;
+    int chunks;  // ceil(m / 32): monomials are evaluated 32 per warp pass
+    int kp;      // row stride of posexp (k rounded up to 8 -> 16-byte rows)
+    // posexp[s*kp + j] = pos | (exp-1) << 8   (the reference's two byte arrays,
+    // ref src/packing.cpp:40-44, fused into one 16-bit word per (s, j))
+    const uint16_t* posexp;
+    // coefficient planes, derivative-major like ref src/packing.cpp:46-49:
+    // component c of (j, s) at coef[(j*W + c)*nm + s]; block j < k = a_j*c, block k = c
+    const double* coef;
+    // stage-3 gather map: entries of Jacobian entry (p, v) from chunk c are
+    // gm_ent[gm_off[(p*chunks + c)*n + v] .. gm_off[... + 1]), ascending g; an entry is
+    // j*32 + (g mod 32), i.e. derivative j of chunk-local monomial g
+    const int* gm_off;
+    const uint16_t* gm_ent;
+};
+
+struct LaunchCfg {
+    int blocks = 0;
+    int threads = 256;
+    int tp = 1;               // points per CTA tile
+    size_t smem_bytes = 0;    // dynamic shared memory (0 in global-scratch mode)
+    double* gscratch = nullptr;  // non-null: tables/staging in global memory (huge systems)
+    int* flag = nullptr;      // device int, set to 1 on a non-finite coordinate
+};
+
+cudaError_t launch_eval(int prec, int order, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out,
+                        long long B, cudaStream_t st);
+int max_blocks_per_sm(int prec, int order, int threads, size_t smem);
+cudaError_t set_smem_attr(size_t bytes);
+
+}  // namespace pjb

@@ -1,0 +1,404 @@
+"""Host-side mirror of the reference's C++ API for the hot path, over the C ABI.
+
+Reference surface (ref = /root/reference/proj):
+  PolynomialSystem / Term / MonomialSupport   ref include/polyjac/system.hpp:14-42
+  validate_system                             ref src/system.cpp:21-64
+  random_system / random_points / random_point ref src/system.cpp:66-118
+  GridConfig                                  ref include/polyjac/engine.hpp:16-19
+  EvaluationContext(sys, grid)                ref src/engine.cpp:168-179
+    .evaluate(point) -> EvaluationResult      ref src/engine.cpp:181-230
+    .evaluate_batch(points, repeat)           ref src/engine.cpp:232-260
+    .mults() / .masked_slots_clean()          ref include/polyjac/engine.hpp:104-108
+  mons_slot / zero_mask / stage2_slot_targets ref src/packing.cpp:8-72, src/kernels.cpp:129-137
+
+Same names, argument meaning and error behaviour (ValueError where the reference throws
+std::invalid_argument, IndexError for std::out_of_range). Additions for the B200 path:
+complex double-double evaluation (`evaluate_dd`, `precision="dd"`) and batched device-tensor
+evaluation (`evaluate_device`) on a CUDA stream. All arithmetic runs in the CUDA kernels of
+libpolyjac_b200.so; nothing here computes results on the CPU.
+"""
+from __future__ import annotations
+
+import ctypes
+import time
+from dataclasses import dataclass, field
+from typing import List, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import PJ_ORDER_FAST, PJ_ORDER_REF, PJ_PREC_D, PJ_PREC_DD, SystemDesc, check, lib
+
+
+# --------------------------------------------------------------------------- system model
+@dataclass
+class MonomialSupport:
+    positions: List[int]
+    exponents: List[int]
+
+    def size(self) -> int:
+        return len(self.positions)
+
+
+@dataclass
+class Term:
+    coeff: complex
+    support: MonomialSupport
+
+
+@dataclass
+class PolynomialSystem:
+    """n polynomials in n variables, m monomials each, k variables per monomial, degrees in
+    [1, d]; terms flat in S_m order (monomial g of polynomial p at p*m + g).
+
+    Stored as arrays: positions/exponents int32 [n*m, k]; coeffs float64 [n*m, 4] =
+    (re_hi, re_lo, im_hi, im_lo) so double-double coefficients are representable."""
+    n: int
+    m: int
+    k: int
+    d: int
+    positions: np.ndarray
+    exponents: np.ndarray
+    coeffs: np.ndarray
+
+    @staticmethod
+    def from_terms(n: int, m: int, k: int, d: int, terms: Sequence[Term]) -> "PolynomialSystem":
+        nt = len(terms)
+        kk = max(k, 0)
+        pos = np.full((nt, kk), -1, np.int32)
+        exps = np.zeros((nt, kk), np.int32)
+        co = np.zeros((nt, 4), np.float64)
+        bad = False
+        for s, t in enumerate(terms):
+            if len(t.support.positions) != k or len(t.support.exponents) != k:
+                bad = True
+                continue
+            pos[s] = t.support.positions
+            exps[s] = t.support.exponents
+            c = complex(t.coeff)
+            co[s] = (c.real, 0.0, c.imag, 0.0)
+        sys = PolynomialSystem(n, m, k, d, pos, exps, co)
+        sys._shape_error = bad or nt != n * m
+        return sys
+
+    def monomial_count(self) -> int:
+        return self.n * self.m
+
+    def term(self, p: int, g: int) -> Term:
+        s = p * self.m + g
+        c = self.coeffs[s]
+        return Term(complex(c[0] + c[1], c[2] + c[3]),
+                    MonomialSupport([int(v) for v in self.positions[s]], [int(v) for v in self.exponents[s]]))
+
+    @property
+    def terms(self) -> List[Term]:
+        return [self.term(s // self.m, s % self.m) for s in range(self.n * self.m)]
+
+    def _desc(self):
+        pos = np.ascontiguousarray(self.positions, np.int32).reshape(-1)
+        exps = np.ascontiguousarray(self.exponents, np.int32).reshape(-1)
+        co = np.ascontiguousarray(self.coeffs, np.float64).reshape(-1)
+        keep = (pos, exps, co)
+        desc = SystemDesc(self.n, self.m, self.k, self.d, pos.ctypes.data, exps.ctypes.data, co.ctypes.data)
+        if getattr(self, "_shape_error", False) or pos.size != self.n * self.m * max(self.k, 0):
+            desc.positions = desc.exponents = desc.coeffs = None  # "term count is not n*m"
+        return desc, keep
+
+
+@dataclass
+class Violation:
+    poly: int
+    mono: int
+    rule: str
+
+    def describe(self) -> str:
+        return self.rule
+
+
+@dataclass
+class ValidationReport:
+    violations: List[Violation] = field(default_factory=list)
+
+    def ok(self) -> bool:
+        return not self.violations
+
+
+def validate_system(sys: PolynomialSystem) -> ValidationReport:
+    desc, keep = sys._desc()
+    buf = ctypes.create_string_buffer(512)
+    nv = lib().pj_validate(ctypes.byref(desc), buf, 512)
+    rep = ValidationReport()
+    if nv > 0:
+        rep.violations.append(Violation(-1, -1, buf.value.decode()))
+        rep.violations.extend(Violation(-1, -1, "") for _ in range(nv - 1))
+    return rep
+
+
+def random_system(n: int, m: int, k: int, d: int, seed: int) -> PolynomialSystem:
+    """Bit-identical to the reference generator (ref src/system.cpp:66-101)."""
+    nm = max(n, 0) * max(m, 0)
+    pos = np.empty((nm, max(k, 1)), np.int32)
+    exps = np.empty((nm, max(k, 1)), np.int32)
+    co = np.empty((nm, 4), np.float64)
+    check(lib().pj_random_system(n, m, k, d, seed, pos.ctypes.data, exps.ctypes.data, co.ctypes.data))
+    return PolynomialSystem(n, m, k, d, pos, exps, co)
+
+
+def random_points(n: int, count: int, seed: int) -> np.ndarray:
+    """count points, complex128 [count, n], one seeded stream (ref src/system.cpp:103-114)."""
+    out = np.empty((count, n, 2), np.float64)
+    check(lib().pj_random_points(n, count, seed, out.ctypes.data))
+    return out.view(np.complex128).reshape(count, n)
+
+
+def random_point(n: int, seed: int) -> np.ndarray:
+    return random_points(n, 1, seed)[0]
+
+
+def to_dd(points) -> np.ndarray:
+    """complex128 [..., n] -> double-double planes float64 [..., n, 4] with zero low words."""
+    z = np.asarray(points, np.complex128)
+    out = np.zeros(z.shape + (4,), np.float64)
+    out[..., 0] = z.real
+    out[..., 2] = z.imag
+    return out
+
+
+def mons_slot(s: int, kind: str, var: int, n: int, m: int) -> int:
+    """ref src/packing.cpp:8-17; IndexError where the reference throws std::out_of_range."""
+    out = ctypes.c_int64(0)
+    check(lib().pj_mons_slot(s, 0 if kind == "value" else 1, var, n, m, ctypes.byref(out)))
+    return out.value
+
+
+def mons_value_slot(s, n, m):
+    return mons_slot(s, "value", -1, n, m)
+
+
+def mons_deriv_slot(s, var, n, m):
+    return mons_slot(s, "derivative", var, n, m)
+
+
+# --------------------------------------------------------------------------- results
+@dataclass
+class GridConfig:
+    block_size: int = 32
+    workers: int = 0  # 0 = all hardware threads (the CPU pool's knob; the GPU grid ignores it)
+
+
+@dataclass
+class EvaluationResult:
+    n: int
+    values: np.ndarray    # complex128 [n]   (dd: float64 [n, 4])
+    jacobian: np.ndarray  # complex128 [n*n] row-major by polynomial (dd: [n*n, 4])
+
+    def jac(self, p: int, i: int):
+        return self.jacobian[p * self.n + i]
+
+
+@dataclass
+class MultCounter:
+    stage1_powers: int = 0
+    stage1_factors: int = 0
+    stage2: int = 0
+    speelpenning: int = 0
+    stage3: int = 0
+
+    def total(self) -> int:
+        return self.stage1_powers + self.stage1_factors + self.stage2 + self.stage3
+
+
+@dataclass
+class BatchReport:
+    evals: int = 0
+    wall_seconds: float = 0.0
+    per_eval_seconds: float = 0.0
+    mults: MultCounter = field(default_factory=MultCounter)
+
+
+@dataclass
+class BatchResult:
+    results: List[EvaluationResult]
+    report: BatchReport
+
+
+def _flags(precision: str, order: str | None) -> int:
+    if precision == "d":
+        return PJ_PREC_D | (PJ_ORDER_FAST if order == "fast" else 0)
+    if precision == "dd":
+        return PJ_PREC_DD | (PJ_ORDER_REF if order == "ref" else 0)
+    raise ValueError(f"unknown precision {precision!r} (expected 'd' or 'dd')")
+
+
+class EvaluationContext:
+    """Owns the packed system on one GPU (uploaded once) and evaluates points there.
+
+    Like the reference, one context must not serve concurrent evaluate calls; use one per
+    thread (or per device / stream)."""
+
+    def __init__(self, sys: PolynomialSystem, grid: GridConfig | None = None, device: int = 0):
+        grid = grid or GridConfig()
+        if grid.block_size < 1:
+            raise ValueError("block size must be >= 1")
+        if grid.workers < 0:
+            raise ValueError("workers must be >= 0")
+        self.grid_ = GridConfig(grid.block_size, grid.workers if grid.workers > 0 else 1)
+        self.n, self.m, self.k, self.d = sys.n, sys.m, sys.k, sys.d
+        self.device = device
+        desc, keep = sys._desc()
+        h = ctypes.c_void_p()
+        check(lib().pj_ctx_create(ctypes.byref(desc), device, ctypes.byref(h)))
+        self._h = h
+        self._mults = MultCounter()
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            try:
+                lib().pj_ctx_destroy(h)
+            except Exception:
+                pass
+            self._h = None
+
+    # ---- reference surface
+    def grid(self) -> GridConfig:
+        return self.grid_
+
+    def mults(self) -> MultCounter:
+        return self._mults
+
+    def masked_slots_clean(self) -> bool:
+        """The padded Mons buffer does not exist on the GPU path: structural zeros are never
+        written, so every masked slot is trivially an exact +0 (ref engine.cpp:262-269)."""
+        return True
+
+    def layout_info(self):
+        n, m, k, d = (ctypes.c_int32() for _ in range(4))
+        fp = ctypes.c_int64()
+        check(lib().pj_layout_info(self._h, ctypes.byref(n), ctypes.byref(m), ctypes.byref(k), ctypes.byref(d),
+                                   ctypes.byref(fp)))
+        return dict(n=n.value, m=m.value, k=k.value, d=d.value, footprint_bytes=fp.value)
+
+    def _tally(self, evals: int) -> MultCounter:
+        c = (ctypes.c_uint64 * 5)()
+        check(lib().pj_mult_counts(self._h, evals, ctypes.addressof(c)))
+        return MultCounter(*[int(v) for v in c])
+
+    def _add_tally(self, evals):
+        t = self._tally(evals)
+        mc = self._mults
+        mc.stage1_powers += t.stage1_powers
+        mc.stage1_factors += t.stage1_factors
+        mc.stage2 += t.stage2
+        mc.speelpenning += t.speelpenning
+        mc.stage3 += t.stage3
+
+    def evaluate_host(self, points: np.ndarray, precision: str = "d", order: str | None = None) -> np.ndarray:
+        """Batched host-buffer evaluation. points: [B, n, W] float64 (W = 2 for 'd', 4 for 'dd');
+        returns [B, n + n*n, W]."""
+        W = 2 if precision == "d" else 4
+        pts = np.ascontiguousarray(points, np.float64)
+        if pts.ndim != 3 or pts.shape[1:] != (self.n, W):
+            raise ValueError("evaluate: point dimension mismatch")
+        B = pts.shape[0]
+        out = np.empty((B, self.n + self.n * self.n, W), np.float64)
+        check(lib().pj_evaluate_host(self._h, _flags(precision, order), pts.ctypes.data, B, out.ctypes.data))
+        self._add_tally(B)
+        return out
+
+    def evaluate(self, point) -> EvaluationResult:
+        """One point (sequence of n complex numbers) in complex double; bit-identical with the
+        reference's EvaluationContext::evaluate."""
+        z = np.asarray(point, np.complex128).reshape(-1)
+        if z.shape[0] != self.n:
+            raise ValueError("evaluate: point dimension mismatch")
+        if not np.all(np.isfinite(z.real) & np.isfinite(z.imag)):
+            raise ValueError("evaluate: non-finite coordinate")
+        pts = np.stack([z.real, z.imag], -1)[None]
+        out = self.evaluate_host(pts, "d")[0]
+        c = out[:, 0] + 1j * out[:, 1]
+        return EvaluationResult(self.n, c[: self.n].copy(), c[self.n:].copy())
+
+    def evaluate_dd(self, points_dd: np.ndarray, order: str | None = None) -> np.ndarray:
+        """Complex double-double: points [B, n, 4] -> [B, n + n*n, 4]."""
+        return self.evaluate_host(points_dd, "dd", order)
+
+    def evaluate_batch(self, points, repeat: int) -> BatchResult:
+        if repeat < 1:
+            raise ValueError("evaluate_batch: repeat must be >= 1")
+        pts = [np.asarray(p, np.complex128).reshape(-1) for p in points]
+        for z in pts:
+            if z.shape[0] != self.n:
+                raise ValueError("evaluate: point dimension mismatch")
+        before = MultCounter(**vars(self._mults))
+        t0 = time.perf_counter()
+        results = []
+        if pts:
+            arr = np.stack([np.stack([z.real, z.imag], -1) for z in pts])
+            out = None
+            for _ in range(repeat):
+                out = self.evaluate_host(arr, "d")
+            c = out[..., 0] + 1j * out[..., 1]
+            results = [EvaluationResult(self.n, c[b, : self.n].copy(), c[b, self.n:].copy()) for b in range(len(pts))]
+        t1 = time.perf_counter()
+        evals = len(pts) * repeat
+        mc = self._mults
+        delta = MultCounter(mc.stage1_powers - before.stage1_powers, mc.stage1_factors - before.stage1_factors,
+                            mc.stage2 - before.stage2, mc.speelpenning - before.speelpenning, mc.stage3 - before.stage3)
+        rep = BatchReport(evals, t1 - t0, (t1 - t0) / evals if evals else 0.0, delta)
+        return BatchResult(results, rep)
+
+    # ---- device path (torch tensors or raw pointers)
+    def evaluate_device(self, points, out, precision: str = "dd", order: str | None = None, stream=None) -> None:
+        """Asynchronous evaluation of device-resident points. points/out: CUDA tensors (or objects
+        with data_ptr()) of shapes [B, n, W] / [B, n + n*n, W], float64, contiguous; stream: a
+        torch.cuda.Stream, a raw cudaStream_t int, or None (torch's current stream)."""
+        W = 2 if precision == "d" else 4
+        B = int(points.shape[0])
+        if tuple(points.shape[1:]) != (self.n, W) or tuple(out.shape) != (B, self.n + self.n * self.n, W):
+            raise ValueError("evaluate_device: shape mismatch")
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(points.device).cuda_stream
+        elif hasattr(stream, "cuda_stream"):
+            stream = stream.cuda_stream
+        check(lib().pj_evaluate(self._h, _flags(precision, order), points.data_ptr(), B, out.data_ptr(),
+                                ctypes.c_void_p(stream)))
+
+    def nonfinite_seen(self, stream=None) -> bool:
+        if hasattr(stream, "cuda_stream"):
+            stream = stream.cuda_stream
+        seen = ctypes.c_int(0)
+        check(lib().pj_nonfinite_seen(self._h, ctypes.c_void_p(stream or 0), ctypes.byref(seen)))
+        return bool(seen.value)
+
+    # ---- index maps (bit-exact with the reference)
+    def slot_targets(self, s: int) -> np.ndarray:
+        out = np.empty(self.k + 1, np.int64)
+        check(lib().pj_slot_targets(self._h, s, out.ctypes.data))
+        return out
+
+    def zero_mask(self) -> np.ndarray:
+        ln = lib().pj_zero_mask(self._h, None, 0)
+        if ln < 0:
+            check(_lib.PJ_EINVAL)
+        out = np.empty(ln, np.int64)
+        lib().pj_zero_mask(self._h, out.ctypes.data, ln)
+        return out
+
+    # ---- launch shape
+    def set_launch(self, precision: str, threads: int = 0, tile_points: int = 0) -> None:
+        check(lib().pj_set_launch(self._h, _flags(precision, None), threads, tile_points))
+
+    def launch(self, precision: str):
+        t, tp, b = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+        sm = ctypes.c_int64()
+        check(lib().pj_get_launch(self._h, _flags(precision, None), ctypes.byref(t), ctypes.byref(tp),
+                                  ctypes.byref(b), ctypes.byref(sm)))
+        return dict(threads=t.value, tile_points=tp.value, blocks=b.value, smem_bytes=sm.value)
+
+
+def fp64_peak_tflops(device: int = 0) -> float:
+    v = ctypes.c_double(0)
+    check(lib().pj_fp64_peak_probe(device, ctypes.byref(v)))
+    return v.value
