@@ -1,0 +1,371 @@
+#!/usr/bin/env python3
+"""Benchmark of the hot path: complex double-double system + Jacobian evaluation.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...        (one rank per GPU)
+
+Workload (BASELINE.json configs[1]): random_system(32, 32, 8, 2, seed 7) (n=32 variables,
+32 polynomials x 32 monomials of k=8 variables, degrees <= 2), a batch of 65,536 points per
+GPU drawn from random_points(32, ., seed 11) — contiguous shards of one stream, so the
+union over ranks is the single-process batch. A step = one evaluation of the batch (values +
+full Jacobian, complex dd). Weak scaling: per-GPU batch fixed; no collective on the data
+path (the barrier and the max-over-ranks timing reduction are the only ones).
+
+One JSON line (rank 0). `value` = evaluations/s over all ranks, device time (CUDA events on
+the launching stream, max over ranks); `e2e` = the same through the public host API
+(pinned host points -> H2D -> kernels -> D2H of every value and Jacobian entry);
+`roofline` = the kernel's algorithmic FP64 rate (SURVEY.md §8d cost model) over the FP64
+peak measured live on this device; `cpu_baseline` = the unmodified reference (compiled from
+/root/reference sources into oracle/_ref) on this host's cores, a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "system+Jacobian evals/sec (complex dd, n=32) and % of FP64 peak, 1/2/4/8 GPUs"
+N, M, K, D, SYS_SEED, PT_SEED = 32, 32, 8, 2, 7, 11
+POINTS_PER_GPU = 65536
+# dd_mul = 10 flops, dd_add = 20, complex dd mul = 80, complex dd add = 40;
+# per eval cmul = n*max(d-2,0) + nm(k-1) + nm(5k-4), cadd = nm(k+1) (useful terms)
+def model_flops(n, m, k, d, prec="dd"):
+    cmul = n * max(d - 2, 0) + n * m * (k - 1) + n * m * (5 * k - 4)
+    cadd = n * m * (k + 1)
+    return cmul * 80 + cadd * 40 if prec == "dd" else cmul * 6 + cadd * 2
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    FIELDS = ["clocks.sm", "clocks.max.sm", "clocks_event_reasons.sw_power_cap", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown"]
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), "--query-gpu=" + ",".join(self.FIELDS),
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], 0.0, set()
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != len(self.FIELDS):
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_count():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def reference_cpu(sysd, n, target_seconds=8.0, threads=None, prec="ref"):
+    """Time the unmodified reference (oracle/_ref, complex double — the reference has no dd) or
+    the oracle's dd restatement (prec="dd-port") point-sharded across host threads (one
+    workers=1 context per thread). Bounded sample sized from a calibration run."""
+    from oracle import oracle as O
+    threads = threads or cpu_count()
+    rng_pts = O.ref_random_points(n, 1, PT_SEED) if O.ref_available() else None
+
+    def run(B):
+        if prec == "ref":
+            pts = O.ref_random_points(n, B, PT_SEED)
+            t0 = time.perf_counter()
+            O.ref_evaluate(sysd, pts, threads=threads)
+            return time.perf_counter() - t0, pts
+        pts2 = O.ref_random_points(n, B, PT_SEED) if O.ref_available() else None
+        p4 = np.zeros((B, n, 4))
+        p4[..., 0], p4[..., 2] = pts2[..., 0], pts2[..., 1]
+        t0 = time.perf_counter()
+        O.evaluate("dd", sysd, p4, threads=threads)
+        return time.perf_counter() - t0, p4
+
+    del rng_pts
+    cal = 32 * threads
+    dt, _ = run(cal)
+    B = int(min(max(cal, cal * target_seconds / max(dt, 1e-6)), 1 << 20))
+    dt, pts = run(B)
+    return B / dt, B, dt, threads, pts
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for ln in fh:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libpolyjac_ref.so not built "
+                          "(needs /root/reference at build time)"}))
+        return 0
+    sysd = O.ref_random_system(N, M, K, D, SYS_SEED)
+    threads = cpu_count()
+    # calibrate once, then size every step so the whole run stays within ~2 minutes
+    # (each step >= ~0.25 s of CPU work so thread start-up does not dominate)
+    cal = 32 * threads
+    pts = O.ref_random_points(N, cal, PT_SEED)
+    t0 = time.perf_counter()
+    O.ref_evaluate(sysd, pts, threads=threads)
+    rate = cal / (time.perf_counter() - t0)
+    step_s = max(0.25, min(args.ref_seconds, 120.0 / (args.warmup + args.steps)))
+    B_used = int(max(cal, min(rate * step_s, 1 << 20)))
+    pts = O.ref_random_points(N, B_used, PT_SEED)
+    vals, dts = [], []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        O.ref_evaluate(sysd, pts, threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= args.warmup:
+            vals.append(B_used / dt)
+            dts.append(dt)
+    value = B_used * len(dts) / sum(dts)
+    dt_used = sum(dts) / len(dts)
+    line = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "impl": "reference", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt_used * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic: reference random_system(32,32,8,2,seed 7), random_points(32, ., seed 11)",
+        "config": {"workload": "C2: n=32 m=32 k=8 d=2, evaluation-point batch (bounded CPU sample)",
+                   "points_per_step": B_used, "parallelism": f"{threads} host threads, point-sharded"},
+        "cpu_baseline": {"value": value, "unit": "evals/s", "cores": threads, "kind": "reference",
+                         "sample": f"{B_used} points per step through the unmodified reference "
+                                   "EvaluationContext::evaluate (complex double: the reference has no "
+                                   f"double-double path), one workers=1 context per thread; {cpu_model()}"},
+        "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--points", type=int, default=POINTS_PER_GPU, help="points per GPU per step")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--ref-seconds", type=float, default=4.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--order", default="fast", choices=["fast", "ref"])
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import paper_1201_0499_b200 as pj
+
+    ws, rank, local = dist_env()
+    dist = ws > 1
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if dist:
+        import torch.distributed as tdist
+        tdist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if dist:
+            tdist.barrier()
+
+    sysobj = pj.random_system(N, M, K, D, SYS_SEED)
+    ctx = pj.EvaluationContext(sysobj, device=local)
+    B = args.points
+    nout = N + N * N
+    # this rank's contiguous shard of the global point stream
+    from paper_1201_0499_b200.sharding import shard_points
+    host_pts = shard_points(N, B * ws, PT_SEED, ws, rank)  # complex128 [B, n]
+    dd = pj.to_dd(host_pts)
+    # inputs > L2: rotate over NBUF distinct device batches (NBUF * 67 MB > 126 MB L2)
+    NBUF = 4
+    bufs = []
+    for i in range(NBUF):
+        t = torch.from_numpy(np.roll(dd, i, axis=0).copy()).to(dev)
+        bufs.append(t)
+    out = torch.empty((B, nout, 4), dtype=torch.float64, device=dev)
+    stream = torch.cuda.Stream(dev)
+    with torch.cuda.stream(stream):
+        for i in range(args.warmup):
+            ctx.evaluate_device(bufs[i % NBUF], out, "dd", args.order, stream)
+    stream.synchronize()
+    if ctx.nonfinite_seen(stream):
+        raise RuntimeError("non-finite input")
+
+    # ---------------- timed region (device): K steps, events on the launching stream
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize(dev)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    with torch.cuda.stream(stream):
+        evs[0].record(stream)
+        for i in range(args.steps):
+            ctx.evaluate_device(bufs[i % NBUF], out, "dd", args.order, stream)
+            evs[i + 1].record(stream)
+    stream.synchronize()
+    torch.cuda.synchronize(dev)
+    barrier()
+    clk = clocks.stop()
+    per = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
+    total_ms = evs[0].elapsed_time(evs[-1])
+    if dist:
+        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    value = B * ws * args.steps / (total_ms * 1e-3)
+    ms_per_step = total_ms / args.steps
+    kern_ms = statistics.mean(per)
+
+    # ---------------- e2e through the public host API (pinned host buffers)
+    pin_in = torch.from_numpy(dd).pin_memory()
+    pin_out = torch.empty((B, nout, 4), dtype=torch.float64).pin_memory()
+    ni, no = pin_in.numpy(), pin_out.numpy()
+    ctx.evaluate_host(ni, "dd", args.order, out=no)  # warm (allocates the staging buffers)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        ctx.evaluate_host(ni, "dd", args.order, out=no)
+    e2e_s = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": B * ws * args.e2e_steps / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": int(ni.nbytes),
+           "d2h_bytes_per_step": int(no.nbytes), "steps": args.e2e_steps,
+           "api": "EvaluationContext.evaluate_host -> pj_evaluate_host (3-stream chunked H2D/kernel/D2H)"}
+
+    # ---------------- roofline: FP64 issue-bound
+    peak = pj.fp64_peak_tflops(local)
+    flops = model_flops(N, M, K, D)
+    achieved = flops * B / (kern_ms * 1e-3) / 1e12
+    io_bytes = B * (N * 32 + nout * 32)
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as fh:
+                traffic = json.load(fh).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": traffic, "algorithmic_bytes": io_bytes,
+                "hbm_gbs_achieved": io_bytes / (kern_ms * 1e-3) / 1e9,
+                "flops_per_eval": flops,
+                "peak_source": "pj_fp64_peak_probe: DFMA throughput measured live on this device (2 flops/DFMA); "
+                               "MEASURED_PEAKS.json carries no FP64 figure"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "complex-dd (f64 pairs)",
+        "data": "synthetic: random_system(32,32,8,2,seed 7), random_points(32, 65536*N, seed 11) sharded by rank",
+        "config": {"workload": "C2: n=32 m=32 k=8 d=2, 65,536 evaluation points per GPU per step",
+                   "points_per_gpu": B, "global_points": B * ws, "order": args.order,
+                   "parallelism": f"points sharded over {ws} GPU(s), system replicated, no collective",
+                   "l2": f"inputs rotate over {NBUF} device batches ({NBUF * dd.nbytes >> 20} MiB > 126 MiB L2); "
+                         f"outputs {B * nout * 32 >> 20} MiB per step",
+                   "launch": ctx.launch("dd")},
+        "roofline": roofline,
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "clocks": clk,
+    }
+
+    # ---------------- CPU baseline (rank 0, N=1 only): the unmodified reference
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            from oracle import oracle as O
+            if O.ref_available():
+                sysd = O.ref_random_system(N, M, K, D, SYS_SEED)
+                v, Bs, dt, thr, pts = reference_cpu(sysd, N, target_seconds=args.ref_seconds)
+                vdd, Bdd, dtdd, _, p4 = reference_cpu(sysd, N, target_seconds=args.ref_seconds / 2, prec="dd-port")
+                line["cpu_baseline"] = {
+                    "value": v, "unit": "evals/s", "cores": thr, "kind": "reference",
+                    "sample": f"{Bs} points of the same workload through the unmodified reference "
+                              f"EvaluationContext::evaluate (complex double — the reference has no dd path), "
+                              f"{thr} threads point-sharded, {dt:.2f} s; {cpu_model()}",
+                    "dd_port": {"value": vdd, "unit": "evals/s", "cores": thr, "kind": "port",
+                                "sample": f"{Bdd} points through the oracle's complex-dd restatement, {dtdd:.2f} s"},
+                }
+                # checker: the GPU result on the CPU sample's first points vs the oracle (dd)
+                chk = min(64, Bdd)
+                want, ms = O.evaluate("dd", sysd, p4[:chk], magsum=True)
+                got = ctx.evaluate_dd(p4[:chk])
+                err = np.maximum(np.abs((got[..., 0] - want[..., 0]) + (got[..., 1] - want[..., 1])),
+                                 np.abs((got[..., 2] - want[..., 2]) + (got[..., 3] - want[..., 3])))
+                line["parity_gate"] = {"points": chk, "max_err_over_sum_abs_terms": float(np.max(err / np.maximum(ms, 1e-300))),
+                                       "tol": 1e-30}
+        except Exception as exc:  # the baseline must never hide the measurement
+            line["cpu_baseline"] = {"error": repr(exc)}
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        tdist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -66,7 +66,8 @@ int pj_validate(const pj_system_desc* sys, char* msg, size_t cap);
 
 /* Context creation: validate + pack + upload once; replaces
  * EvaluationContext::EvaluationContext(sys, GridConfig), ref src/engine.cpp:168-179 and
- * build_layout, ref src/packing.cpp:19-52 (PJ_EINVAL for an invalid system or n > 256). */
+ * build_layout, ref src/packing.cpp:19-52 (PJ_EINVAL for an invalid system or n > 256).
+ * device < 0 creates a host-only context (packing and index maps, no evaluation). */
 int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out);
 void pj_ctx_destroy(pj_ctx* ctx);
 
@@ -108,6 +109,9 @@ int pj_mult_counts(const pj_ctx* ctx, int64_t evals, uint64_t* counts);
 int pj_random_system(int n, int m, int k, int d, uint64_t seed, int32_t* positions, int32_t* exponents,
                      double* coeffs);
 int pj_random_points(int n, int64_t count, uint64_t seed, double* points);
+/* Points [first, first + count) of the same stream (a contiguous shard of random_points(n, N,
+ * seed) for any N >= first + count): lets each rank generate only its own shard. */
+int pj_random_points_range(int n, int64_t first, int64_t count, uint64_t seed, double* points);
 
 /* Advanced: override the launch shape for `flags`' precision (threads per CTA, multiple of 32,
  * <= 256; points per CTA tile). 0 restores the automatic choice. */

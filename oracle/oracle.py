@@ -24,6 +24,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libpolyjac_ref.so")
+DROPIN_BIN = os.path.join(HERE, "_ref", "test_dropin")
 REF_SRC = "/root/reference/proj"
 
 _i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
@@ -38,6 +39,9 @@ def build(ref: bool | None = None) -> None:
         ref = os.path.isdir(REF_SRC)
     if ref:
         subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
+        # the C++ drop-in check links the product library; build it only once that exists
+        if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_1201_0499_b200", "libpolyjac_b200.so")):
+            subprocess.run(["make", "-s", "-C", HERE, "dropin"], check=True)
 
 
 _oracle = None

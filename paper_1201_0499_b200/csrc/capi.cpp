@@ -103,6 +103,7 @@ struct PrecState {
 
 struct pj_ctx {
     int device = 0;
+    bool host_only = false;
     int sms = 0;
     size_t smem_optin = 0;
     int n, m, k, d, kp, chunks;
@@ -116,11 +117,14 @@ struct pj_ctx {
     PrecState prec[2];  // [0] = d, [1] = dd
     double* d_scratch = nullptr;
     size_t scratch_bytes = 0;
-    // host-API staging buffers
-    double* d_in = nullptr;
-    double* d_out = nullptr;
+    // host-API pipeline: kHostStreams streams, each with its own device staging buffers, so
+    // H2D of chunk i+1, the kernel on chunk i and D2H of chunk i-1 overlap
+    static constexpr int kHostStreams = 3;
+    double* d_in[kHostStreams] = {};
+    double* d_out[kHostStreams] = {};
     size_t in_cap = 0, out_cap = 0;
-    cudaStream_t hstream = nullptr;
+    cudaStream_t hstream[kHostStreams] = {};
+    cudaEvent_t hdone[kHostStreams] = {};
 
     pjb::DevSystem dev(int pi) const {
         pjb::DevSystem S;
@@ -143,6 +147,10 @@ namespace {
 
 void free_ctx(pj_ctx* c) {
     if (!c) return;
+    if (c->host_only) {
+        delete c;
+        return;
+    }
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
@@ -153,9 +161,12 @@ void free_ctx(pj_ctx* c) {
     cudaFree(c->prec[0].coef);
     cudaFree(c->prec[1].coef);
     cudaFree(c->d_scratch);
-    cudaFree(c->d_in);
-    cudaFree(c->d_out);
-    if (c->hstream) cudaStreamDestroy(c->hstream);
+    for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
+        cudaFree(c->d_in[i]);
+        cudaFree(c->d_out[i]);
+        if (c->hstream[i]) cudaStreamDestroy(c->hstream[i]);
+        if (c->hdone[i]) cudaEventDestroy(c->hdone[i]);
+    }
     cudaSetDevice(prev);
     delete c;
 }
@@ -321,6 +332,12 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
                 }
     }
 
+    if (device < 0) {  // host-only context: packing and index maps, no device residency
+        c->host_only = true;
+        g_err.clear();
+        *out = c;
+        return PJ_OK;
+    }
     int prev = 0;
     cudaGetDevice(&prev);
     cudaError_t e = cudaSetDevice(device);
@@ -340,11 +357,19 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
         (e = up((void**)&c->prec[1].coef, cdd.data(), cdd.size() * 8)) ||
         (e = up((void**)&c->d_gm_off, c->gm_off.data(), c->gm_off.size() * 4)) ||
         (e = up((void**)&c->d_gm_ent, c->gm_ent.data(), c->gm_ent.size() * 2)) ||
-        (e = cudaMalloc((void**)&c->d_flag, sizeof(int))) || (e = cudaMemset(c->d_flag, 0, sizeof(int))) ||
-        (e = cudaStreamCreateWithFlags(&c->hstream, cudaStreamNonBlocking))) {
+        (e = cudaMalloc((void**)&c->d_flag, sizeof(int))) || (e = cudaMemset(c->d_flag, 0, sizeof(int)))) {
         free_ctx(c);
         cudaSetDevice(prev);
         return cuda_fail(e, "pj_ctx_create: device upload");
+    }
+    for (int i = 0; i < pj_ctx::kHostStreams && !e; ++i) {
+        e = cudaStreamCreateWithFlags(&c->hstream[i], cudaStreamNonBlocking);
+        if (!e) e = cudaEventCreateWithFlags(&c->hdone[i], cudaEventDisableTiming);
+    }
+    if (e) {
+        free_ctx(c);
+        cudaSetDevice(prev);
+        return cuda_fail(e, "pj_ctx_create: streams");
     }
     c->sms = prop.multiProcessorCount;
     c->smem_optin = prop.sharedMemPerBlockOptin;
@@ -389,6 +414,7 @@ int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, d
         return PJ_OK;
     }
     if (!d_points || !d_out) return fail(PJ_EINVAL, "evaluate: null buffer");
+    if (ctx->host_only) return fail(PJ_EINVAL, "evaluate: host-only context (created with device < 0)");
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != ctx->device) PJ_CUDA(cudaSetDevice(ctx->device));
@@ -402,6 +428,7 @@ int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, d
 
 int pj_nonfinite_seen(pj_ctx* ctx, void* stream, int* seen) {
     if (!ctx || !seen) return fail(PJ_EINVAL, "null argument");
+    if (ctx->host_only) return fail(PJ_EINVAL, "host-only context");
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != ctx->device) PJ_CUDA(cudaSetDevice(ctx->device));
@@ -429,36 +456,57 @@ int pj_evaluate_host(pj_ctx* ctx, int flags, const double* h_points, int64_t bat
         return PJ_OK;
     }
     if (!h_points || !h_out) return fail(PJ_EINVAL, "evaluate: null buffer");
+    if (ctx->host_only) return fail(PJ_EINVAL, "evaluate: host-only context (created with device < 0)");
     const int W = pi == 0 ? 2 : 4;
-    const size_t in_b = size_t(batch) * ctx->n * W * 8;
-    const size_t out_b = size_t(batch) * (size_t(ctx->n) * ctx->n + ctx->n) * W * 8;
+    const size_t in_pt = size_t(ctx->n) * W * 8;
+    const size_t out_pt = (size_t(ctx->n) * ctx->n + ctx->n) * W * 8;
+    // chunk: large enough to fill every SM for several waves, small enough that the D2H of
+    // one chunk overlaps the kernel of the next (pinned host buffers give full overlap)
+    const pjb::LaunchCfg& L = ctx->prec[pi].cfg;
+    int64_t chunk = std::max<int64_t>(int64_t(L.blocks) * L.tp * 4, 1024);
+    chunk = std::max<int64_t>(chunk, int64_t((256ull << 20) / out_pt));
+    chunk = std::min<int64_t>(chunk, batch);
+    const int nchunks = int((batch + chunk - 1) / chunk);
+    const int ns = std::min(nchunks, int(pj_ctx::kHostStreams));
     int prev = 0;
     cudaGetDevice(&prev);
     PJ_CUDA(cudaSetDevice(ctx->device));
-    if (in_b > ctx->in_cap) {
-        cudaFree(ctx->d_in);
-        ctx->d_in = nullptr;
-        ctx->in_cap = 0;
-        PJ_CUDA(cudaMalloc(&ctx->d_in, in_b));
-        ctx->in_cap = in_b;
+    if (size_t(chunk) * in_pt > ctx->in_cap || size_t(chunk) * out_pt > ctx->out_cap) {
+        for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
+            cudaFree(ctx->d_in[i]);
+            cudaFree(ctx->d_out[i]);
+            ctx->d_in[i] = ctx->d_out[i] = nullptr;
+        }
+        ctx->in_cap = ctx->out_cap = 0;
+        for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
+            PJ_CUDA(cudaMalloc(&ctx->d_in[i], size_t(chunk) * in_pt));
+            PJ_CUDA(cudaMalloc(&ctx->d_out[i], size_t(chunk) * out_pt));
+        }
+        ctx->in_cap = size_t(chunk) * in_pt;
+        ctx->out_cap = size_t(chunk) * out_pt;
     }
-    if (out_b > ctx->out_cap) {
-        cudaFree(ctx->d_out);
-        ctx->d_out = nullptr;
-        ctx->out_cap = 0;
-        PJ_CUDA(cudaMalloc(&ctx->d_out, out_b));
-        ctx->out_cap = out_b;
+    int rc = PJ_OK;
+    for (int c = 0; c < nchunks && rc == PJ_OK; ++c) {
+        const int si = c % ns;
+        cudaStream_t st = ctx->hstream[si];
+        const int64_t b0 = int64_t(c) * chunk, nb = std::min<int64_t>(chunk, batch - b0);
+        PJ_CUDA(cudaMemcpyAsync(ctx->d_in[si], reinterpret_cast<const char*>(h_points) + size_t(b0) * in_pt,
+                                size_t(nb) * in_pt, cudaMemcpyHostToDevice, st));
+        rc = pj_evaluate(ctx, flags, ctx->d_in[si], nb, ctx->d_out[si], st);
+        if (rc) break;
+        PJ_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(h_out) + size_t(b0) * out_pt, ctx->d_out[si],
+                                size_t(nb) * out_pt, cudaMemcpyDeviceToHost, st));
     }
-    cudaStream_t st = ctx->hstream;
-    PJ_CUDA(cudaMemcpyAsync(ctx->d_in, h_points, in_b, cudaMemcpyHostToDevice, st));
-    int rc = pj_evaluate(ctx, flags, ctx->d_in, batch, ctx->d_out, st);
+    for (int i = 0; i < ns; ++i) {
+        cudaError_t e = cudaStreamSynchronize(ctx->hstream[i]);
+        if (e && rc == PJ_OK) rc = cuda_fail(e, "evaluate_host: stream");
+    }
     if (rc) {
         cudaSetDevice(prev);
         return rc;
     }
-    PJ_CUDA(cudaMemcpyAsync(h_out, ctx->d_out, out_b, cudaMemcpyDeviceToHost, st));
     int seen = 0;
-    rc = pj_nonfinite_seen(ctx, st, &seen);
+    rc = pj_nonfinite_seen(ctx, ctx->hstream[0], &seen);
     cudaSetDevice(prev);
     if (rc) return rc;
     if (seen) return fail(PJ_ENONFINITE, "evaluate: non-finite coordinate");
@@ -597,8 +645,13 @@ int pj_random_system(int n, int m, int k, int d, uint64_t seed, int32_t* positio
 }
 
 int pj_random_points(int n, int64_t count, uint64_t seed, double* points) {
-    if (n < 1 || count < 0) return fail(PJ_EINVAL, "random_points: bad shape");
+    return pj_random_points_range(n, 0, count, seed, points);
+}
+
+int pj_random_points_range(int n, int64_t first, int64_t count, uint64_t seed, double* points) {
+    if (n < 1 || count < 0 || first < 0) return fail(PJ_EINVAL, "random_points: bad shape");
     Gen r(seed);
+    r.e.discard(uint64_t(first) * uint64_t(n) * 2);
     for (int64_t i = 0; i < count * n; ++i) {
         points[2 * i] = r.sym();
         points[2 * i + 1] = r.sym();
@@ -609,6 +662,7 @@ int pj_random_points(int n, int64_t count, uint64_t seed, double* points) {
 
 int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points) {
     if (!ctx) return fail(PJ_EINVAL, "null context");
+    if (ctx->host_only) return fail(PJ_EINVAL, "host-only context");
     const int pi = prec_index(flags);
     if (pi < 0) return fail(PJ_EINVAL, "unknown precision flag");
     if (threads < 0 || threads > 256 || threads % 32) return fail(PJ_EINVAL, "threads must be a multiple of 32 <= 256");

@@ -293,15 +293,21 @@ class EvaluationContext:
         mc.speelpenning += t.speelpenning
         mc.stage3 += t.stage3
 
-    def evaluate_host(self, points: np.ndarray, precision: str = "d", order: str | None = None) -> np.ndarray:
+    def evaluate_host(self, points: np.ndarray, precision: str = "d", order: str | None = None,
+                      out: np.ndarray | None = None) -> np.ndarray:
         """Batched host-buffer evaluation. points: [B, n, W] float64 (W = 2 for 'd', 4 for 'dd');
-        returns [B, n + n*n, W]."""
+        returns [B, n + n*n, W] (written into `out` when given — pass page-locked buffers, e.g.
+        torch pin_memory() tensors' .numpy(), for full H2D/kernel/D2H overlap)."""
         W = 2 if precision == "d" else 4
         pts = np.ascontiguousarray(points, np.float64)
         if pts.ndim != 3 or pts.shape[1:] != (self.n, W):
             raise ValueError("evaluate: point dimension mismatch")
         B = pts.shape[0]
-        out = np.empty((B, self.n + self.n * self.n, W), np.float64)
+        shape = (B, self.n + self.n * self.n, W)
+        if out is None:
+            out = np.empty(shape, np.float64)
+        elif out.shape != shape or out.dtype != np.float64 or not out.flags.c_contiguous:
+            raise ValueError("evaluate: output buffer must be C-contiguous float64 of shape %s" % (shape,))
         check(lib().pj_evaluate_host(self._h, _flags(precision, order), pts.ctypes.data, B, out.ctypes.data))
         self._add_tally(B)
         return out

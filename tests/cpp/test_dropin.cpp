@@ -1,0 +1,118 @@
+// Drop-in check of the C++ surface (include/polyjac_b200.hpp) against the UNMODIFIED reference,
+// using the reference's own types: the same polyjac::PolynomialSystem goes into
+// polyjac::EvaluationContext (reference, CPU) and polyjac_b200::EvaluationContext (B200), and
+// the results must be bit-identical. Mirrors ref tests/test_engine.cpp. Built by
+// `make -C oracle dropin` (compiles the reference sources where they lie) into oracle/_ref/;
+// run by tests/test_gpu_dropin.py on a GPU box. Test infrastructure only.
+#include <cmath>
+#include <cstdio>
+#include <limits>
+#include <stdexcept>
+#include <string>
+
+#include "polyjac/engine.hpp"
+#include "polyjac/oracle.hpp"
+#include "polyjac_b200.hpp"
+
+static int g_fail = 0, g_pass = 0;
+#define CHECK(cond)                                                             \
+    do {                                                                        \
+        if (cond) {                                                             \
+            ++g_pass;                                                           \
+        } else {                                                                \
+            ++g_fail;                                                           \
+            std::printf("FAIL %s:%d: %s\n", __FILE__, __LINE__, #cond);        \
+        }                                                                       \
+    } while (0)
+template <class E, class F>
+static bool throws(F f) {
+    try {
+        f();
+    } catch (const E&) {
+        return true;
+    } catch (...) {
+        return false;
+    }
+    return false;
+}
+
+static bool bit_equal(const polyjac::EvaluationResult& a, const polyjac::EvaluationResult& b) {
+    if (a.n != b.n || a.values.size() != b.values.size() || a.jacobian.size() != b.jacobian.size()) return false;
+    for (size_t i = 0; i < a.values.size(); ++i)
+        if (!polyjac::bit_equal(a.values[i], b.values[i])) return false;
+    for (size_t i = 0; i < a.jacobian.size(); ++i)
+        if (!polyjac::bit_equal(a.jacobian[i], b.jacobian[i])) return false;
+    return true;
+}
+
+int main() {
+    using namespace polyjac;
+    // engine shapes of ref tests/test_engine.cpp:70-83 and acceptance criterion 1 corners
+    const int shapes[][4] = {{32, 32, 9, 2}, {32, 32, 16, 10}, {8, 3, 3, 5}, {4, 4, 1, 1}, {40, 40, 20, 3},
+                             {4, 1, 1, 255}, {32, 32, 8, 2}, {64, 64, 16, 10}, {10, 40, 4, 3}};
+    std::uint64_t seed = 7000;
+    for (auto& s : shapes) {
+        const PolynomialSystem sys = random_system(s[0], s[1], s[2], s[3], seed++);
+        EvaluationContext ref(sys, {32, 1});
+        polyjac_b200::EvaluationContext gpu(sys);
+        for (int t = 0; t < 3; ++t) {
+            const EvaluationPoint pt = random_point(s[0], seed++);
+            CHECK(bit_equal(gpu.evaluate<EvaluationResult>(pt), ref.evaluate(pt)));
+        }
+        // batch + multiplication tallies equal to the reference's counters
+        const auto pts = random_points(s[0], 5, seed++);
+        auto rb = ref.evaluate_batch(pts, 2);
+        auto gb = gpu.evaluate_batch<EvaluationResult>(pts, 2);
+        CHECK(gb.report.evals == rb.report.evals);
+        CHECK(gb.report.mults.total() == rb.report.mults.total());
+        CHECK(gb.report.mults.speelpenning == rb.report.mults.speelpenning);
+        bool all = gb.results.size() == rb.results.size();
+        for (size_t i = 0; all && i < gb.results.size(); ++i) all = bit_equal(gb.results[i], rb.results[i]);
+        CHECK(all);
+    }
+    // ref tests/test_engine.cpp:298-305: point validation
+    {
+        const PolynomialSystem sys = random_system(4, 2, 2, 2, 8);
+        polyjac_b200::EvaluationContext ctx(sys);
+        CHECK(throws<std::invalid_argument>([&] { ctx.evaluate(EvaluationPoint(3, Complex{1.0, 0.0})); }));
+        EvaluationPoint bad(4, Complex{1.0, 0.0});
+        bad[2].im = std::numeric_limits<double>::quiet_NaN();
+        CHECK(throws<std::invalid_argument>([&] { ctx.evaluate(bad); }));
+        CHECK(throws<std::invalid_argument>([&] { ctx.evaluate_batch(std::vector<EvaluationPoint>{}, 0); }));
+        // the context keeps working after a rejected point
+        CHECK(ctx.evaluate<EvaluationResult>(EvaluationPoint(4, Complex{1.0, 0.0})).n == 4);
+    }
+    // ref tests/test_engine.cpp:385-391 and packing rejections
+    {
+        const PolynomialSystem sys = random_system(4, 2, 2, 2, 3);
+        CHECK(throws<std::invalid_argument>([&] { polyjac_b200::EvaluationContext c(sys, {0, 1}); }));
+        CHECK(throws<std::invalid_argument>([&] { polyjac_b200::EvaluationContext c(sys, {32, -1}); }));
+        PolynomialSystem bad = sys;
+        bad.terms[0].coeff = {0.0, 0.0};
+        CHECK(throws<std::invalid_argument>([&] { polyjac_b200::EvaluationContext c(bad); }));
+        PolynomialSystem wide{300, 1, 1, 1, {}};
+        for (int p = 0; p < 300; ++p) wide.terms.push_back({{1.0, 0.0}, {{p}, {1}}});
+        CHECK(throws<std::invalid_argument>([&] { polyjac_b200::EvaluationContext c(wide); }));
+        PolynomialSystem shortsys = sys;
+        shortsys.terms.pop_back();
+        CHECK(throws<std::invalid_argument>([&] { polyjac_b200::EvaluationContext c(shortsys); }));
+    }
+    // ref tests/test_engine.cpp:181-196 in complex dd: integer answers are exact
+    {
+        PolynomialSystem sys{2, 2, 2, 1, {}};
+        const Term t{{0.5, 0.0}, {{0, 1}, {1, 1}}};
+        sys.terms = {t, t, t, t};
+        polyjac_b200::EvaluationContext ctx(sys);
+        polyjac_b200::ComplexDD pt[2] = {{3, 0, 0, 0}, {5, 0, 0, 0}};
+        polyjac_b200::ComplexDD out[6];
+        ctx.evaluate_dd(pt, 1, out);
+        CHECK(out[0].re_hi == 15 && out[0].re_lo == 0);
+        CHECK(out[2].re_hi == 5 && out[3].re_hi == 3);
+        ctx.evaluate_dd(pt, 1, out, /*reference_order=*/true);
+        CHECK(out[0].re_hi == 15 && out[2].re_hi == 5 && out[3].re_hi == 3);
+        auto r = ctx.evaluate<EvaluationResult>(EvaluationPoint{{3.0, 0.0}, {5.0, 0.0}});
+        CHECK(compare(r, sys, {{3.0, 0.0}, {5.0, 0.0}}, 1e-10).pass);
+    }
+    std::printf("%s: %d passed, %d failed\n", g_fail ? "FAIL" : "PASS", g_pass, g_fail);
+    return g_fail ? 1 : 0;
+}
