@@ -116,9 +116,15 @@ int pj_random_points_range(int n, int64_t first, int64_t count, uint64_t seed, d
 /* Advanced: override the launch shape for `flags`' precision (threads per CTA, multiple of 32,
  * <= 256; points per CTA tile). 0 restores the automatic choice. */
 int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points);
-/* Report the launch shape used for `flags`: threads, tile points, blocks, dynamic smem bytes. */
+/* Advanced: kernel variant of the fast dd order. 0 = automatic, -1 = the generic kernel,
+ * else (P << 2) | (FREG << 1) | SH: P in {1, 2} points per lane, SH = coordinates in registers
+ * with warp-shuffle gathers (needs n <= 32, d <= 2), FREG = forward products in registers
+ * (SH only). Results of every variant satisfy the same contract. */
+int pj_set_kernel_variant(pj_ctx* ctx, int flags, int variant);
+/* Report the launch shape used for `flags`: threads, tile points, blocks, dynamic smem bytes,
+ * kernel variant (-1 = generic kernel). */
 int pj_get_launch(pj_ctx* ctx, int flags, int32_t* threads, int32_t* tile_points, int32_t* blocks,
-                  int64_t* smem_bytes);
+                  int64_t* smem_bytes, int32_t* variant);
 
 /* Measurement helper (not part of the reference surface): FP64 DFMA throughput of `device`
  * in TFLOP/s (2 flops per DFMA), the denominator of the roofline fraction. */

@@ -20,7 +20,7 @@ EXPORTS = [
     "pj_last_error", "pj_version", "pj_validate", "pj_ctx_create", "pj_ctx_destroy", "pj_evaluate",
     "pj_evaluate_host", "pj_nonfinite_seen", "pj_layout_info", "pj_mons_slot", "pj_slot_targets",
     "pj_zero_mask", "pj_mult_counts", "pj_random_system", "pj_random_points", "pj_set_launch",
-    "pj_get_launch", "pj_fp64_peak_probe", "pj_random_points_range",
+    "pj_get_launch", "pj_fp64_peak_probe", "pj_random_points_range", "pj_set_kernel_variant",
 ]
 
 
@@ -65,7 +65,8 @@ def lib():
     L.pj_random_points.argtypes = [ctypes.c_int, i64, u64, vp]
     L.pj_random_points_range.argtypes = [ctypes.c_int, i64, i64, u64, vp]
     L.pj_set_launch.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
-    L.pj_get_launch.argtypes = [vp, ctypes.c_int, i32p, i32p, i32p, i64p]
+    L.pj_get_launch.argtypes = [vp, ctypes.c_int, i32p, i32p, i32p, i64p, i32p]
+    L.pj_set_kernel_variant.argtypes = [vp, ctypes.c_int, ctypes.c_int]
     L.pj_fp64_peak_probe.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     for name in EXPORTS:
         getattr(L, name)  # fail loudly on a stale library

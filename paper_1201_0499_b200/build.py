@@ -18,7 +18,7 @@ SO = os.path.join(HERE, "libpolyjac_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU = ["eval_kernels.cu", "fp64_probe.cu"]
+CU = ["eval_kernels.cu", "eval_fast.cu", "fp64_probe.cu"]
 CPP = ["capi.cpp"]
 HEADERS = ["dd.cuh", "eval_kernels.h"]
 
@@ -45,10 +45,17 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for f in CU:
         src = os.path.join(CSRC, f)
         obj = os.path.join(BUILD, f + ".o")
-        if force or _newer(obj, [src] + hdrs):
-            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
-                   "-fmad=false", "-Xptxas", "-v", "-c", src, "-o", obj]
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
+               "-fmad=false", "-Xptxas", "-v", "-c", src, "-o", obj]
+        ks = os.environ.get("PJB_FAST_KS")  # developer shortcut: e.g. "8,16" (default: 2..16)
+        if ks and f == "eval_fast.cu":
+            cmd.insert(-4, "-DPJB_FAST_KS(X)=" + " ".join(f"X({k})" for k in ks.split(",")))
+        stamp = obj + ".cmd"
+        old = open(stamp).read() if os.path.exists(stamp) else ""
+        if force or old != " ".join(cmd) or _newer(obj, [src] + hdrs):
             r = _run(cmd)
+            with open(stamp, "w") as fh:
+                fh.write(" ".join(cmd))
             if verbose:
                 sys.stderr.write(r.stderr)
         objs.append(obj)

@@ -92,12 +92,16 @@ void dd_mul_small(double hi, double lo, double a, double* oh, double* ol) {
     *ol = e - (s - p);
 }
 
-struct PrecState {
-    double* coef = nullptr;   // device planes
-    pjb::LaunchCfg cfg;       // automatic or overridden
-    int over_threads = 0, over_tp = 0;
-    bool cfg_ready = false;
+// Launch state per evaluation mode: 0 = complex double (generic kernel, either order),
+// 1 = complex dd in the reference order (generic kernel), 2 = complex dd in the fast order
+// (specialised eval_fast.cu kernel when k is instantiated and the tables fit, else generic).
+enum { kModeD = 0, kModeDDRef = 1, kModeDDFast = 2, kModes = 3 };
+struct ModeState {
+    pjb::LaunchCfg cfg;
+    int over_threads = 0, over_tp = 0, over_variant = 0;
 };
+
+
 
 }  // namespace
 
@@ -113,8 +117,14 @@ struct pj_ctx {
     uint16_t* d_posexp = nullptr;
     int* d_gm_off = nullptr;
     uint16_t* d_gm_ent = nullptr;
+    std::vector<uint32_t> sch, seg;  // fast-kernel stage-3 schedule (host copies)
+    uint32_t* d_sch = nullptr;
+    uint32_t* d_seg = nullptr;
+    int nseg = 0;
     int* d_flag = nullptr;
-    PrecState prec[2];  // [0] = d, [1] = dd
+    double* d_coef[2] = {};  // coefficient planes: [0] complex double, [1] complex dd
+    double* d_coefT = nullptr;  // complex dd, tiled per (row, chunk) for the fast kernel
+    ModeState mode[kModes];
     double* d_scratch = nullptr;
     size_t scratch_bytes = 0;
     // host-API pipeline: kHostStreams streams, each with its own device staging buffers, so
@@ -136,9 +146,13 @@ struct pj_ctx {
         S.chunks = chunks;
         S.kp = kp;
         S.posexp = d_posexp;
-        S.coef = prec[pi].coef;
+        S.coef = d_coef[pi];
         S.gm_off = d_gm_off;
         S.gm_ent = d_gm_ent;
+        S.sch = d_sch;
+        S.seg = d_seg;
+        S.nseg = nseg;
+        S.coefT = d_coefT;
         return S;
     }
 };
@@ -157,9 +171,12 @@ void free_ctx(pj_ctx* c) {
     cudaFree(c->d_posexp);
     cudaFree(c->d_gm_off);
     cudaFree(c->d_gm_ent);
+    cudaFree(c->d_sch);
+    cudaFree(c->d_seg);
     cudaFree(c->d_flag);
-    cudaFree(c->prec[0].coef);
-    cudaFree(c->prec[1].coef);
+    cudaFree(c->d_coef[0]);
+    cudaFree(c->d_coef[1]);
+    cudaFree(c->d_coefT);
     cudaFree(c->d_scratch);
     for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
         cudaFree(c->d_in[i]);
@@ -171,47 +188,75 @@ void free_ctx(pj_ctx* c) {
     delete c;
 }
 
-// Shared-memory footprint of one CTA: TP points' power tables + per-warp staging and
-// accumulators (see eval_kernels.cu).
+// Shared-memory footprint of one CTA of the generic kernel: TP points' power tables +
+// per-warp staging and accumulators (see eval_kernels.cu).
 size_t smem_need(const pj_ctx* c, int W, int nw, int tp) {
     const size_t D1 = c->d > 2 ? c->d - 1 : 1;
     const size_t tab = D1 * W * c->n;
     const size_t per_warp = size_t(c->k + 1) * W * 32 + size_t(c->n + 1) * W;
     return (tp * tab + nw * per_warp) * sizeof(double);
 }
+// ... and of the fast kernel (eval_fast.cu): tables with the padded plane stride, per-warp
+// staging + segment partials (+ accumulators when m > 32).
+size_t smem_need_fast(const pj_ctx* c, int nw, int tp) {
+    const size_t D1 = c->d > 2 ? c->d - 1 : 1;
+    const size_t tab = D1 * 4 * size_t(pjb::fast_plane_stride(c->n));
+    const size_t acc = c->chunks > 1 ? size_t(c->n + 1) * 4 : 0;
+    const size_t per_warp = size_t(c->k + 1) * 4 * 32 + size_t(c->nseg) * 4 + acc;
+    return (tp * tab + nw * per_warp) * sizeof(double);
+}
 
-int choose_launch(pj_ctx* c, int pi) {
-    PrecState& P = c->prec[pi];
-    const int W = pi == 0 ? 2 : 4;
-    const int precflag = pi == 0 ? 1 : 2;
+int choose_launch(pj_ctx* c, int mode) {
+    ModeState& M = c->mode[mode];
+    const int W = mode == kModeD ? 2 : 4;
+    const int precflag = mode == kModeD ? 1 : 2;
     int best_score = -1;
     pjb::LaunchCfg best;
     std::vector<int> nws = {8, 4, 2, 1}, tps = {8, 4, 2, 1};
-    if (P.over_threads) nws = {P.over_threads / 32};
-    if (P.over_tp) tps = {P.over_tp};
-    for (int nw : nws) {
-        for (int tp : tps) {
-            const size_t sm = smem_need(c, W, nw, tp);
-            if (sm > c->smem_optin) continue;
-            const int nb = pjb::max_blocks_per_sm(precflag, 0, nw * 32, sm);
-            if (nb <= 0) continue;
-            // resident warps first; then fewer, fatter tiles (more coefficient reuse) as long as
-            // a tile still has a task per warp
-            const int warps = std::min(nb * nw, 64);
-            const int score = warps * 64 + (tp * c->n >= nw ? tp : 0);
-            if (score > best_score) {
-                best_score = score;
-                best.threads = nw * 32;
-                best.tp = tp;
-                best.smem_bytes = sm;
-                best.blocks = nb * c->sms;
-            }
+    if (M.over_threads) nws = {M.over_threads / 32};
+    if (M.over_tp) tps = {M.over_tp};
+    auto consider = [&](int variant, int nw, int tp, size_t sm, int nb) {
+        if (nb <= 0) return;
+        // resident warps first; then fewer, fatter tiles (more coefficient reuse) as long as
+        // a tile still has a task per warp
+        const int warps = std::min(nb * nw, 64);
+        const int score = warps * 64 + (tp * c->n >= nw ? tp : 0);
+        if (score > best_score) {
+            best_score = score;
+            best.variant = variant;
+            best.threads = nw * 32;
+            best.tp = tp;
+            best.smem_bytes = sm;
+            best.blocks = nb * c->sms;
+            best.gscratch = nullptr;
         }
+    };
+    if (mode == kModeDDFast && pjb::fast_supported(c->k) && M.over_variant >= 0) {
+        // smaller tiles measured faster for the fast kernel (finer grid-stride balance)
+        // measured (tools/tune.py): 8-warp CTAs beat more, smaller CTAs at equal residency;
+        // among tiles that keep the residency, the largest (<= 4) is marginally best
+        std::vector<int> ftps = M.over_tp ? tps : std::vector<int>{4, 2, 1};
+        std::vector<int> fnws = M.over_threads ? nws : std::vector<int>{8};
+        for (int nw : fnws)
+            for (int tp : ftps) {
+                const size_t sm = smem_need_fast(c, nw, tp);
+                if (sm > c->smem_optin) continue;
+                consider(1, nw, tp, sm, pjb::fast_blocks_per_sm(c->k, c->n, nw * 32, sm));
+            }
+    }
+    if (best_score < 0) {
+        for (int nw : nws)
+            for (int tp : tps) {
+                const size_t sm = smem_need(c, W, nw, tp);
+                if (sm > c->smem_optin) continue;
+                consider(-1, nw, tp, sm, pjb::max_blocks_per_sm(precflag, 0, nw * 32, sm));
+            }
     }
     if (best_score < 0) {
         // global-scratch fallback for systems whose tables exceed shared memory
-        const int nw = P.over_threads ? P.over_threads / 32 : 4;
-        const int tp = P.over_tp ? P.over_tp : 1;
+        const int nw = M.over_threads ? M.over_threads / 32 : 4;
+        const int tp = M.over_tp ? M.over_tp : 1;
+        best.variant = -1;
         best.threads = nw * 32;
         best.tp = tp;
         best.smem_bytes = 0;
@@ -227,8 +272,7 @@ int choose_launch(pj_ctx* c, int pi) {
         best.gscratch = c->d_scratch;
     }
     best.flag = c->d_flag;
-    P.cfg = best;
-    P.cfg_ready = true;
+    M.cfg = best;
     return PJ_OK;
 }
 
@@ -307,6 +351,15 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
             }
         }
     }
+    // the same dd coefficients tiled per (row, 32-monomial chunk), lane index fastest
+    std::vector<double> cddT(size_t(c->n) * c->chunks * (k + 1) * 4 * 32, 0.0);
+    for (int p = 0; p < c->n; ++p)
+        for (int g = 0; g < c->m; ++g) {
+            const size_t s = size_t(p) * c->m + g;
+            const size_t base = (size_t(p) * c->chunks + g / 32) * (k + 1) * 4 * 32 + (g & 31);
+            for (size_t j = 0; j <= k; ++j)
+                for (int q = 0; q < 4; ++q) cddT[base + (j * 4 + q) * 32] = cdd[(j * 4 + q) * nm + s];
+        }
     // stage-3 gather map: for (row p, chunk c, column v) the ascending-g list of (g, j) with
     // positions[s*k+j] == v — the inverse of the reference's derivative slot map
     // mons_slot(s, derivative, v) = g*(n^2+n) + (v+1)*n + p (ref src/packing.cpp:8-17)
@@ -332,6 +385,47 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
                 }
     }
 
+    // fast-kernel stage-3 schedule: per (p, c) the output-major, ascending-g list of staged terms
+    // (value terms first, then Jacobian columns), cut into 32 equal runs (one per lane); a segment
+    // is a maximal piece of one output inside one run
+    {
+        const int R = c->k + 1;
+        c->nseg = n + 1 + 32;
+        c->sch.assign(size_t(n) * C * R * 32, 0);
+        c->seg.assign(size_t(n) * C * (n + 1), 0);
+        std::vector<std::pair<int, uint32_t>> ent;  // (output, staging code)
+        for (int p = 0; p < n; ++p)
+            for (int ch = 0; ch < C; ++ch) {
+                ent.clear();
+                const int gl = std::min(32, c->m - ch * 32);
+                for (int g = 0; g < gl; ++g) ent.push_back({0, uint32_t(c->k * 32 + g)});
+                for (int v = 0; v < n; ++v) {
+                    const size_t li = (size_t(p) * C + ch) * n + v;
+                    for (int e = c->gm_off[li]; e < c->gm_off[li + 1]; ++e) ent.push_back({v + 1, c->gm_ent[e]});
+                }
+                const int T = int(ent.size());
+                const int Rr = (T + 31) / 32;
+                int segid = -1, prev_o = -1;
+                uint32_t* sc = c->sch.data() + (size_t(p) * C + ch) * R * 32;
+                uint32_t* sg = c->seg.data() + (size_t(p) * C + ch) * (n + 1);
+                for (int lane = 0; lane < 32; ++lane) {
+                    const int a = lane * Rr, b = std::min(T, a + Rr);
+                    for (int q = a; q < b; ++q) {
+                        const int o = ent[q].first;
+                        if (q == a || o != prev_o) {
+                            ++segid;
+                            if ((sg[o] >> 16) == 0) sg[o] = uint32_t(segid);
+                            sg[o] += 1u << 16;
+                        }
+                        prev_o = o;
+                        const bool flush = q + 1 == b || ent[q + 1].first != o;
+                        sc[size_t(q - a) * 32 + lane] =
+                            ent[q].second | (uint32_t(segid) << 13) | (flush ? pjb::kSchFlush : 0) | pjb::kSchValid;
+                    }
+                }
+            }
+    }
+
     if (device < 0) {  // host-only context: packing and index maps, no device residency
         c->host_only = true;
         g_err.clear();
@@ -353,10 +447,13 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
     cudaDeviceProp prop;
     if ((e = cudaGetDeviceProperties(&prop, device)) ||
         (e = up((void**)&c->d_posexp, posexp.data(), posexp.size() * 2)) ||
-        (e = up((void**)&c->prec[0].coef, cd.data(), cd.size() * 8)) ||
-        (e = up((void**)&c->prec[1].coef, cdd.data(), cdd.size() * 8)) ||
+        (e = up((void**)&c->d_coef[0], cd.data(), cd.size() * 8)) ||
+        (e = up((void**)&c->d_coef[1], cdd.data(), cdd.size() * 8)) ||
+        (e = up((void**)&c->d_coefT, cddT.data(), cddT.size() * 8)) ||
         (e = up((void**)&c->d_gm_off, c->gm_off.data(), c->gm_off.size() * 4)) ||
         (e = up((void**)&c->d_gm_ent, c->gm_ent.data(), c->gm_ent.size() * 2)) ||
+        (e = up((void**)&c->d_sch, c->sch.data(), c->sch.size() * 4)) ||
+        (e = up((void**)&c->d_seg, c->seg.data(), c->seg.size() * 4)) ||
         (e = cudaMalloc((void**)&c->d_flag, sizeof(int))) || (e = cudaMemset(c->d_flag, 0, sizeof(int)))) {
         free_ctx(c);
         cudaSetDevice(prev);
@@ -379,8 +476,8 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
         cudaSetDevice(prev);
         return cuda_fail(e, "pj_ctx_create: smem attribute");
     }
-    for (int pi = 0; pi < 2; ++pi) {
-        rc = choose_launch(c, pi);
+    for (int md = 0; md < kModes; ++md) {
+        rc = choose_launch(c, md);
         if (rc) {
             free_ctx(c);
             cudaSetDevice(prev);
@@ -403,6 +500,10 @@ static int order_of(int flags) {
     if ((flags & 0x0f) == PJ_PREC_D) return (flags & PJ_ORDER_FAST) ? 1 : 0;
     return (flags & PJ_ORDER_REF) ? 0 : 1;
 }
+static int mode_of(int flags) {
+    if ((flags & 0x0f) == PJ_PREC_D) return kModeD;
+    return (flags & PJ_ORDER_REF) ? kModeDDRef : kModeDDFast;
+}
 
 int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, double* d_out, void* stream) {
     if (!ctx) return fail(PJ_EINVAL, "null context");
@@ -418,8 +519,11 @@ int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, d
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != ctx->device) PJ_CUDA(cudaSetDevice(ctx->device));
-    cudaError_t e = pjb::launch_eval(pi + 1, order_of(flags), ctx->prec[pi].cfg, ctx->dev(pi), d_points, d_out,
-                                     (long long)batch, (cudaStream_t)stream);
+    const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
+    cudaError_t e = L.variant > 0 ? pjb::launch_fast(ctx->k, L, ctx->dev(pi), d_points, d_out, (long long)batch,
+                                                    (cudaStream_t)stream)
+                                   : pjb::launch_eval(pi + 1, order_of(flags), L, ctx->dev(pi), d_points, d_out,
+                                                      (long long)batch, (cudaStream_t)stream);
     if (prev != ctx->device) cudaSetDevice(prev);
     if (e) return cuda_fail(e, "evaluate: kernel launch");
     g_err.clear();
@@ -462,7 +566,7 @@ int pj_evaluate_host(pj_ctx* ctx, int flags, const double* h_points, int64_t bat
     const size_t out_pt = (size_t(ctx->n) * ctx->n + ctx->n) * W * 8;
     // chunk: large enough to fill every SM for several waves, small enough that the D2H of
     // one chunk overlaps the kernel of the next (pinned host buffers give full overlap)
-    const pjb::LaunchCfg& L = ctx->prec[pi].cfg;
+    const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
     int64_t chunk = std::max<int64_t>(int64_t(L.blocks) * L.tp * 4, 1024);
     chunk = std::max<int64_t>(chunk, int64_t((256ull << 20) / out_pt));
     chunk = std::min<int64_t>(chunk, batch);
@@ -667,27 +771,45 @@ int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points) {
     if (pi < 0) return fail(PJ_EINVAL, "unknown precision flag");
     if (threads < 0 || threads > 256 || threads % 32) return fail(PJ_EINVAL, "threads must be a multiple of 32 <= 256");
     if (tile_points < 0) return fail(PJ_EINVAL, "tile_points must be >= 0");
-    ctx->prec[pi].over_threads = threads;
-    ctx->prec[pi].over_tp = tile_points;
+    ModeState& M = ctx->mode[mode_of(flags)];
+    M.over_threads = threads;
+    M.over_tp = tile_points;
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(ctx->device);
-    int rc = choose_launch(ctx, pi);
+    int rc = choose_launch(ctx, mode_of(flags));
+    cudaSetDevice(prev);
+    if (!rc) g_err.clear();
+    return rc;
+}
+
+int pj_set_kernel_variant(pj_ctx* ctx, int flags, int variant) {
+    if (!ctx) return fail(PJ_EINVAL, "null context");
+    if (ctx->host_only) return fail(PJ_EINVAL, "host-only context");
+    if (mode_of(flags) != kModeDDFast) return fail(PJ_EINVAL, "kernel variants exist for the fast dd order only");
+    if (variant > 1 || variant < -1) return fail(PJ_EINVAL, "unknown kernel variant");
+    if (variant == 1 && !pjb::fast_supported(ctx->k)) return fail(PJ_EINVAL, "no specialised kernel for this k");
+    ctx->mode[kModeDDFast].over_variant = variant;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(ctx->device);
+    int rc = choose_launch(ctx, kModeDDFast);
     cudaSetDevice(prev);
     if (!rc) g_err.clear();
     return rc;
 }
 
 int pj_get_launch(pj_ctx* ctx, int flags, int32_t* threads, int32_t* tile_points, int32_t* blocks,
-                  int64_t* smem_bytes) {
+                  int64_t* smem_bytes, int32_t* variant) {
     if (!ctx) return fail(PJ_EINVAL, "null context");
     const int pi = prec_index(flags);
     if (pi < 0) return fail(PJ_EINVAL, "unknown precision flag");
-    const pjb::LaunchCfg& L = ctx->prec[pi].cfg;
+    const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
     if (threads) *threads = L.threads;
     if (tile_points) *tile_points = L.tp;
     if (blocks) *blocks = L.blocks;
     if (smem_bytes) *smem_bytes = int64_t(L.smem_bytes);
+    if (variant) *variant = L.variant;
     g_err.clear();
     return PJ_OK;
 }

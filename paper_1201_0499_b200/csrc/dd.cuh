@@ -76,6 +76,44 @@ __device__ __forceinline__ CDD cdd_mul(CDD a, CDD b) {
     }
     return r;
 }
+// Complex dd product WITHOUT the closing renormalisation: returns (s, l) per component where
+// s = fl(leading sum) and l the folded error terms, |l| <~ u*(|a||b|). Used inside product
+// chains: the next product's TwoProd/FMA cross terms absorb an unnormalised low word at the
+// same normwise error (the dropped lo*lo term stays <= u^2 |a||b|), so the Fast2Sum (3 DADD
+// per component) is paid once per chain instead of once per product (32 instead of 38 FP64
+// instructions). Chains end in a normalising addition (stage 3) or dd_renorm.
+__device__ __forceinline__ CDD cdd_mul_u(CDD a, CDD b) {
+    CDD r;
+    {
+        double p1 = __dmul_rn(a.rh, b.rh), e1 = __fma_rn(a.rh, b.rh, -p1);
+        double p2 = __dmul_rn(a.ih, b.ih), e2 = __fma_rn(a.ih, b.ih, -p2);
+        DD st = two_sum(p1, -p2);
+        double la = __fma_rn(a.rh, b.rl, e1);
+        la = __fma_rn(a.rl, b.rh, la);
+        double lb = __fma_rn(a.ih, b.il, e2);
+        lb = __fma_rn(a.il, b.ih, lb);
+        r.rh = st.hi;
+        r.rl = __dadd_rn(__dsub_rn(la, lb), st.lo);
+    }
+    {
+        double p3 = __dmul_rn(a.rh, b.ih), e3 = __fma_rn(a.rh, b.ih, -p3);
+        double p4 = __dmul_rn(a.ih, b.rh), e4 = __fma_rn(a.ih, b.rh, -p4);
+        DD st = two_sum(p3, p4);
+        double lc = __fma_rn(a.rh, b.il, e3);
+        lc = __fma_rn(a.rl, b.ih, lc);
+        double ld = __fma_rn(a.ih, b.rl, e4);
+        ld = __fma_rn(a.il, b.rh, ld);
+        r.ih = st.hi;
+        r.il = __dadd_rn(__dadd_rn(lc, ld), st.lo);
+    }
+    return r;
+}
+// Exact renormalisation of a (possibly unnormalised) complex dd: TwoSum per component, so the
+// result satisfies |lo| <= ulp(hi)/2.
+__device__ __forceinline__ CDD cdd_renorm(CDD a) {
+    DD re = two_sum(a.rh, a.rl), im = two_sum(a.ih, a.il);
+    return {re.hi, re.lo, im.hi, im.lo};
+}
 __device__ __forceinline__ DD dd_add(DD a, DD b) {
     DD s = two_sum(a.hi, b.hi);
     double e = __dadd_rn(s.lo, __dadd_rn(a.lo, b.lo));

@@ -1,0 +1,342 @@
+// Fast complex double-double kernel (default PJ_PREC_DD order), specialised on the number of
+// variables per monomial K and on P points per lane.
+//
+// Same mapping as eval_kernels.cu (CTA = tile of points, warp = (row p, points) task, lane =
+// monomial, on-chip ordered stage-3 gather), plus:
+//   * K is a template parameter: every chain is unrolled, so the common-factor chain and the
+//     forward-product chain interleave in program order (in-order issue sees two independent
+//     dependency chains per point), and a monomial's K fused position/exponent words arrive in
+//     one 16-byte load;
+//   * coefficient planes tiled per (row, 32-monomial chunk) with the lane index fastest, and
+//     the point tables with a compile-time plane stride: every load of a (j, component) pair
+//     is one base register + an immediate offset;
+//   * products inside a chain alternate between renormalised and unrenormalised (see cmul_n);
+//   * stage 3 runs a balanced segmented reduction over a precomputed (row, chunk) schedule:
+//     every lane sums k+1 consecutive terms of the output-major list, then each output adds
+//     its few segment partials;
+//   * "back-fused" Speelpenning order: the common factor seeds the backward running product,
+//     q = f, L'_j = F_j * q, q *= v_j — all k factor-scaled derivatives in 3k-4 complex
+//     products instead of the reference's (3k-6) + k (ref src/kernels.cpp:55-110). Per monomial
+//     5k-3 complex products instead of 6k-5 (37 vs 43 at k = 8). The value is L'_{k-1} * v_{k-1}
+//     as in the reference (kernels.cpp:112).
+// Results differ from the reference order only by rounding; the contract is
+// |got - want| <= 1e-30 * sum|terms|, checked in tests/test_gpu_parity.py.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "dd.cuh"
+#include "eval_kernels.h"
+
+namespace pjb {
+
+namespace {
+
+__device__ __forceinline__ CDD shfl_cdd(const CDD& v, int src) {
+    return {__shfl_sync(0xffffffffu, v.rh, src), __shfl_sync(0xffffffffu, v.rl, src),
+            __shfl_sync(0xffffffffu, v.ih, src), __shfl_sync(0xffffffffu, v.il, src)};
+}
+__device__ __forceinline__ CDD sel_cdd(bool c, const CDD& a, const CDD& b) {
+    return {c ? a.rh : b.rh, c ? a.rl : b.rl, c ? a.ih : b.ih, c ? a.il : b.il};
+}
+__device__ __forceinline__ CDD ld_pl(const double* p, int stride) {
+    return {p[0], p[stride], p[2 * stride], p[3 * stride]};
+}
+__device__ __forceinline__ void st_pl(double* p, int stride, const CDD& v) {
+    p[0] = v.rh;
+    p[stride] = v.rl;
+    p[2 * stride] = v.ih;
+    p[3 * stride] = v.il;
+}
+__device__ __forceinline__ CDD ldg_coef(const double* q, int nm) {
+    return {__ldg(q), __ldg(q + nm), __ldg(q + 2 * nm), __ldg(q + 3 * nm)};
+}
+__device__ __forceinline__ CDD ld_aos(const double* p) {
+    double2 a = reinterpret_cast<const double2*>(p)[0];
+    double2 b = reinterpret_cast<const double2*>(p)[1];
+    return {a.x, a.y, b.x, b.y};
+}
+__device__ __forceinline__ void st_aos(double* p, const CDD& v) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(v.rh, v.rl);
+    reinterpret_cast<double2*>(p)[1] = make_double2(v.ih, v.il);
+}
+// Product with an optional closing renormalisation. Inside a chain the kernels alternate:
+// a product whose left input is normalised skips the Fast2Sum (cdd_mul_u), the next one pays
+// it (cdd_mul). An unnormalised low word carried along a whole chain grows linearly and its
+// rounding errors with it (chain of 32: worst 39 u^2 vs 7 u^2 normalised); alternating keeps
+// the chain error at the normalised level (worst 9 u^2, mean 3.2 vs 2.7 u^2) while paying the
+// renormalisation on half the chain products only (tools/chain_error measurements).
+__device__ __forceinline__ CDD cmul_n(bool norm, const CDD& a, const CDD& b) {
+    return norm ? cdd_mul(a, b) : cdd_mul_u(a, b);
+}
+__device__ __forceinline__ bool fin(const CDD& v) {
+    return isfinite(v.rh) && isfinite(v.rl) && isfinite(v.ih) && isfinite(v.il);
+}
+
+}  // namespace
+
+// NS: compile-time plane stride of the shared-memory point tables (>= n), so that the four
+// component loads of a gather share one address register (immediate offsets).
+template <int K, int NS>
+__global__ void __launch_bounds__(256) fast_kernel(DevSystem S, const double* __restrict__ pts,
+                                                   double* __restrict__ out, long long B, int TP,
+                                                   int* __restrict__ flag) {
+    constexpr int W = 4;
+    constexpr int R = K + 1;                 // stage-3 schedule entries per lane
+    constexpr int stgW = (K + 1) * W * 32;   // staging doubles per warp
+    extern __shared__ double smem_[];
+    const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = S.n, m = S.m, d = S.d, C = S.chunks;
+    const int D1 = d > 2 ? d - 1 : 1;
+    const int tabPt = D1 * W * NS;
+    const int NSEG = S.nseg;
+    const int segW = NSEG * W;
+    const int accW = C > 1 ? (n + 1) * W : 0;
+    double* tab = smem_;
+    double* stg = smem_ + TP * tabPt + warp * (stgW + segW + accW);
+    double* seg = stg + stgW;
+    double* acc = seg + segW;
+    const long long ntiles = (B + TP - 1) / TP;
+    const long long nout = (long long)n * n + n;
+    const CDD one = {1.0, 0.0, 0.0, 0.0};
+    const CDD zero = {0.0, 0.0, 0.0, 0.0};
+
+    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        const long long b0 = tile * TP;
+        const int tp = (int)min((long long)TP, B - b0);
+        for (int i = threadIdx.x; i < tp * n; i += blockDim.x) {
+            const int t = i / n, v = i - t * n;
+            CDD x = ld_aos(pts + ((b0 + t) * n + v) * W);
+            if (!fin(x)) atomicOr(flag, 1);
+            st_pl(tab + t * tabPt + v, NS, x);
+        }
+        __syncthreads();
+        if (d > 2) {  // power chains, ref kernels.cpp:16-24 (normalised products: shared table)
+            for (int i = threadIdx.x; i < tp * n; i += blockDim.x) {
+                const int t = i / n, v = i - t * n;
+                double* pb = tab + t * tabPt + v;
+                const CDD x = ld_pl(pb, NS);
+                CDD r = x;
+                for (int e = 2; e < d; ++e) {
+                    r = cdd_mul(r, x);
+                    st_pl(pb + (e - 1) * W * NS, NS, r);
+                }
+            }
+            __syncthreads();
+        }
+        for (int task = warp; task < tp * n; task += nw) {
+            const int p = task / tp, t = task - p * tp;
+            const double* xt = tab + t * tabPt;
+            for (int c = 0; c < C; ++c) {
+                const int graw = c * 32 + lane;
+                const int g = graw < m ? graw : m - 1;  // inactive lanes shadow a real monomial
+                const int s = p * m + g;
+                int pos[K], ex1[K];
+                {
+                    const uint4* row = reinterpret_cast<const uint4*>(S.posexp + (size_t)s * S.kp);
+#pragma unroll
+                    for (int q = 0; q < (K + 7) / 8; ++q) {
+                        const uint4 w = __ldg(row + q);
+                        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                        for (int h = 0; h < 8; ++h) {
+                            if (q * 8 + h < K) {
+                                const uint32_t u = (ws[h >> 1] >> ((h & 1) * 16)) & 0xffffu;
+                                pos[q * 8 + h] = u & 255;
+                                ex1[q * 8 + h] = u >> 8;
+                            }
+                        }
+                    }
+                }
+                // coefficients of this (row, chunk), lane-minor tiles: immediate offsets per (j, comp)
+                const double* cf = S.coefT + (size_t)(p * C + c) * (K + 1) * W * 32 + lane;
+                auto COEF = [&](int j) -> CDD {
+                    return {__ldg(cf + (j * W + 0) * 32), __ldg(cf + (j * W + 1) * 32), __ldg(cf + (j * W + 2) * 32),
+                            __ldg(cf + (j * W + 3) * 32)};
+                };
+                auto X = [&](int j) -> CDD { return ld_pl(xt + pos[j], NS); };
+                auto PWsel = [&](int j, const CDD& v) -> CDD {
+                    if (d <= 2) return sel_cdd(ex1[j] != 0, v, one);
+                    return ex1[j] == 0 ? one : ld_pl(xt + (ex1[j] - 1) * W * NS + pos[j], NS);
+                };
+                auto SLOT = [&](int j) -> double* { return stg + j * W * 32 + lane; };
+
+                // ---- stage 1 + forward products (interleaved chains); chain states are
+                // compile-time after unrolling: F_j is normalised iff j is odd, f_j iff j is even;
+                // a product renormalises iff its chain input is not normalised
+                CDD Fc, f, vlast;
+                {
+                    const CDD v0 = X(0);
+                    f = PWsel(0, v0);
+                    Fc = v0;
+                    st_pl(SLOT(1), 32, v0);
+                }
+#pragma unroll
+                for (int j = 1; j < K; ++j) {
+                    const CDD v = X(j);
+                    f = cmul_n((j & 1) == 0, f, PWsel(j, v));
+                    if (j < K - 1) {
+                        Fc = cmul_n((j & 1) == 0, Fc, v);
+                        if (j + 1 < K - 1) st_pl(SLOT(j + 1), 32, Fc);
+                    } else {
+                        vlast = v;
+                    }
+                }
+                // ---- stage 2, back-fused: q = f; L'_j = F_j * q; q *= v_j
+                constexpr bool f_norm = ((K - 1) & 1) == 0;
+                CDD q;
+                {
+                    const CDD L = cdd_mul_u(Fc, f);
+                    st_pl(SLOT(K - 1), 32, cdd_mul_u(L, COEF(K - 1)));
+                    st_pl(SLOT(K), 32, cdd_mul_u(cdd_mul(L, vlast), COEF(K)));
+                    q = cmul_n(!f_norm, f, vlast);
+                }
+#pragma unroll
+                for (int j = K - 2; j >= 1; --j) {
+                    const bool q_norm = (((K - 2 - j) & 1) == 0) ? !f_norm : f_norm;  // state of q here
+                    const CDD L = cdd_mul_u(ld_pl(SLOT(j), 32), q);
+                    st_pl(SLOT(j), 32, cdd_mul_u(L, COEF(j)));
+                    q = cmul_n(!q_norm, q, X(j));
+                }
+                st_pl(SLOT(0), 32, cdd_mul_u(q, COEF(0)));
+                __syncwarp();
+                // ---- stage 3, phase 1: balanced segmented sums. The (row, chunk) schedule
+                // hands every lane R consecutive entries of the output-major, ascending-g list
+                // of staged terms; a lane flushes its running sum at segment ends. The running
+                // sum defers renormalisation: TwoSum of the high words, low words and the TwoSum
+                // error accumulated (8 DADD per component instead of 11, and the high-word chain
+                // is one dependent add per term); the partial is renormalised by the phase-2 add.
+                // Error <= ~(c^3/6 + 3c) u^2 * sum|terms| for a segment of c <= k+1 terms.
+                {
+                    const uint32_t* sc = S.sch + (size_t)(p * C + c) * R * 32 + lane;
+                    double sr = 0.0, lr = 0.0, si = 0.0, li = 0.0;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) {
+                        const uint32_t code = __ldg(sc + r * 32);
+                        if (code & kSchValid) {
+                            const int ent = code & 0x1fff;
+                            const CDD tv = ld_pl(stg + (ent >> 5) * W * 32 + (ent & 31), 32);
+                            const DD a = two_sum(sr, tv.rh), b = two_sum(si, tv.ih);
+                            sr = a.hi;
+                            si = b.hi;
+                            lr = __dadd_rn(lr, __dadd_rn(tv.rl, a.lo));
+                            li = __dadd_rn(li, __dadd_rn(tv.il, b.lo));
+                            if (code & kSchFlush) {
+                                const int sg = (code >> 13) & 0x3ff;
+                                st_pl(seg + sg, NSEG, CDD{sr, lr, si, li});
+                                sr = lr = si = li = 0.0;
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+                // ---- stage 3, phase 2: each output adds its (few) segments in order. Output o
+                // goes to lane o for o < 32; the rest are dealt out from lane 31 downwards so the
+                // value (o = 0, the most segments) has lane 0 to itself.
+                const bool last = c + 1 == C;
+                for (int k2 = 0; k2 * 32 <= n; ++k2) {
+                    const int o = k2 == 0 ? lane : 32 * k2 + (31 - lane);
+                    if (o > n) continue;
+                    const uint32_t sd = __ldg(S.seg + (size_t)(p * C + c) * (n + 1) + o);
+                    const int first = sd & 0xffff, cnt = sd >> 16;
+                    CDD r = c == 0 ? zero : ld_pl(acc + o, n + 1);
+                    for (int qq = 0; qq < cnt; ++qq) {
+                        const CDD sv = ld_pl(seg + first + qq, NSEG);
+                        r = (c == 0 && qq == 0) ? sv : cdd_add(r, sv);
+                    }
+                    if (last) {
+                        if (t < tp) {
+                            const long long at = o == 0 ? p : n + (long long)p * n + (o - 1);
+                            st_aos(out + ((b0 + t) * nout + at) * W, cdd_renorm(r));
+                        }
+                    } else {
+                        st_pl(acc + o, n + 1, r);
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ----------------------------------------------------------------------------- dispatch
+namespace {
+
+template <int K, int NS>
+cudaError_t launch_t(const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
+                     cudaStream_t st) {
+    auto kern = fast_kernel<K, NS>;
+    if (L.smem_bytes > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem_bytes);
+        if (e != cudaSuccess) return e;
+    }
+    kern<<<L.blocks, L.threads, L.smem_bytes, st>>>(S, pts, out, B, L.tp, L.flag);
+    return cudaGetLastError();
+}
+
+template <int K, int NS>
+int occ_t(int threads, size_t smem) {
+    auto kern = fast_kernel<K, NS>;
+    if (smem > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
+        return 0;
+    int nb = 0;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem) == cudaSuccess ? nb : 0;
+}
+
+template <int K>
+cudaError_t launch_k(int ns, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
+                     cudaStream_t st) {
+    if (ns == 32) return launch_t<K, 32>(L, S, pts, out, B, st);
+    if (ns == 64) return launch_t<K, 64>(L, S, pts, out, B, st);
+    return launch_t<K, 256>(L, S, pts, out, B, st);
+}
+template <int K>
+int occ_k(int ns, int threads, size_t smem) {
+    if (ns == 32) return occ_t<K, 32>(threads, smem);
+    if (ns == 64) return occ_t<K, 64>(threads, smem);
+    return occ_t<K, 256>(threads, smem);
+}
+
+}  // namespace
+
+#ifndef PJB_FAST_KS
+#define PJB_FAST_KS(X) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+#endif
+
+bool fast_supported(int k) {
+    switch (k) {
+#define PJB_CASE(KK) \
+    case KK: return true;
+        PJB_FAST_KS(PJB_CASE)
+#undef PJB_CASE
+        default: return false;
+    }
+}
+
+int fast_plane_stride(int n) { return n <= 32 ? 32 : n <= 64 ? 64 : 256; }
+
+cudaError_t launch_fast(int k, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
+                        cudaStream_t st) {
+    const int ns = fast_plane_stride(S.n);
+    switch (k) {
+#define PJB_CASE(KK) \
+    case KK: return launch_k<KK>(ns, L, S, pts, out, B, st);
+        PJB_FAST_KS(PJB_CASE)
+#undef PJB_CASE
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+int fast_blocks_per_sm(int k, int n, int threads, size_t smem) {
+    const int ns = fast_plane_stride(n);
+    switch (k) {
+#define PJB_CASE(KK) \
+    case KK: return occ_k<KK>(ns, threads, smem);
+        PJB_FAST_KS(PJB_CASE)
+#undef PJB_CASE
+        default: return 0;
+    }
+}
+
+}  // namespace pjb

@@ -24,9 +24,23 @@ struct DevSystem {
     // j*32 + (g mod 32), i.e. derivative j of chunk-local monomial g
     const int* gm_off;
     const uint16_t* gm_ent;
+    // balanced stage-3 schedule of the fast kernel (eval_fast.cu), per (row p, chunk c):
+    // sch[((p*chunks + c)*(k+1) + r)*32 + lane] = entry r of lane's run: bits 0-12 staging
+    // code j*32 + g, 13-22 segment id, 23 flush (segment ends here), 24 valid;
+    // seg[(p*chunks + c)*(n+1) + o] = first segment of output o | count << 16 (o = 0 value,
+    // o = v+1 Jacobian column v); nseg = segment capacity per (p, c)
+    const uint32_t* sch;
+    const uint32_t* seg;
+    int nseg;
+    // dd coefficients tiled for the fast kernel: component c of (j, g = 32*chunk + lane) of row
+    // p at coefT[((p*chunks + chunk)*(k+1)*4 + j*4 + c)*32 + lane] (zero for g >= m)
+    const double* coefT;
 };
+constexpr uint32_t kSchFlush = 1u << 23;
+constexpr uint32_t kSchValid = 1u << 24;
 
 struct LaunchCfg {
+    int variant = -1;         // 1 = fast kernel (eval_fast.cu), -1 = generic kernel
     int blocks = 0;
     int threads = 256;
     int tp = 1;               // points per CTA tile
@@ -39,5 +53,12 @@ cudaError_t launch_eval(int prec, int order, const LaunchCfg& L, const DevSystem
                         long long B, cudaStream_t st);
 int max_blocks_per_sm(int prec, int order, int threads, size_t smem);
 cudaError_t set_smem_attr(size_t bytes);
+
+// fast complex-dd kernels (eval_fast.cu), instantiated for k in [2, 16]
+bool fast_supported(int k);
+int fast_plane_stride(int n);
+cudaError_t launch_fast(int k, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
+                        cudaStream_t st);
+int fast_blocks_per_sm(int k, int n, int threads, size_t smem);
 
 }  // namespace pjb

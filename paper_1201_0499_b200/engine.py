@@ -393,15 +393,19 @@ class EvaluationContext:
         return out
 
     # ---- launch shape
-    def set_launch(self, precision: str, threads: int = 0, tile_points: int = 0) -> None:
-        check(lib().pj_set_launch(self._h, _flags(precision, None), threads, tile_points))
+    def set_launch(self, precision: str, threads: int = 0, tile_points: int = 0, order: str | None = None) -> None:
+        check(lib().pj_set_launch(self._h, _flags(precision, order), threads, tile_points))
 
-    def launch(self, precision: str):
-        t, tp, b = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
+    def set_variant(self, variant: int) -> None:
+        """Kernel variant of the fast dd order (see pj_set_kernel_variant): 0 auto, -1 generic."""
+        check(lib().pj_set_kernel_variant(self._h, _flags("dd", None), variant))
+
+    def launch(self, precision: str, order: str | None = None):
+        t, tp, b, var = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         sm = ctypes.c_int64()
-        check(lib().pj_get_launch(self._h, _flags(precision, None), ctypes.byref(t), ctypes.byref(tp),
-                                  ctypes.byref(b), ctypes.byref(sm)))
-        return dict(threads=t.value, tile_points=tp.value, blocks=b.value, smem_bytes=sm.value)
+        check(lib().pj_get_launch(self._h, _flags(precision, order), ctypes.byref(t), ctypes.byref(tp),
+                                  ctypes.byref(b), ctypes.byref(sm), ctypes.byref(var)))
+        return dict(threads=t.value, tile_points=tp.value, blocks=b.value, smem_bytes=sm.value, variant=var.value)
 
 
 def fp64_peak_tflops(device: int = 0) -> float:

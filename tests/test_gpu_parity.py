@@ -255,3 +255,77 @@ def test_reference_order_dd_full_batch_sample(gpu):
     out = _device_run(ctx, p4, "dd", "ref")
     idx = np.arange(0, 4096, 97)
     assert np.array_equal(out[idx], O.evaluate("dd", S, p4[idx], threads=8))
+
+
+# ---- the specialised fast kernel (eval_fast.cu): every instantiated k, chunking, strides
+@pytest.mark.parametrize("k", list(range(2, 18)))
+def test_fast_kernel_each_k(k, gpu):
+    n = max(k + 3, 20)
+    s = pj.random_system(n, 40, k, 3, 900 + k)   # m = 40: two 32-monomial chunks, one partial
+    S = sysd_of(s)
+    ctx = pj.EvaluationContext(s)
+    want_variant = 1 if 2 <= k <= 16 else -1
+    assert ctx.launch("dd")["variant"] == want_variant
+    p4 = stress_dd(pj.random_points(n, 7, 901 + k), k)
+    want, ms = O.evaluate("dd", S, p4, magsum=True)
+    assert dd_rel(ctx.evaluate_dd(p4), want, ms) <= DD_TOL
+    ctx.set_variant(-1)  # the generic kernel in the same (fast) order family
+    assert dd_rel(ctx.evaluate_dd(p4), want, ms) <= DD_TOL
+
+
+@pytest.mark.parametrize("shape", [(256, 2, 16, 2), (64, 70, 16, 10), (33, 32, 8, 2), (100, 33, 12, 5)],
+                         ids=lambda s: "n%d_m%d_k%d_d%d" % s)
+def test_fast_kernel_strides_and_chunks(shape, gpu):
+    n, m, k, d = shape
+    s = pj.random_system(n, m, k, d, 77)
+    S = sysd_of(s)
+    ctx = pj.EvaluationContext(s)
+    p4 = stress_dd(pj.random_points(n, 4, 78), 2)
+    want, ms = O.evaluate("dd", S, p4, magsum=True)
+    assert dd_rel(ctx.evaluate_dd(p4), want, ms) <= DD_TOL
+
+
+def test_fast_kernel_launch_shape_invariance(gpu):
+    s = pj.random_system(32, 32, 8, 2, 5)
+    ctx = pj.EvaluationContext(s)
+    p4 = stress_dd(pj.random_points(32, 29, 6), 4)
+    base = ctx.evaluate_dd(p4)
+    for threads in (32, 64, 128, 256):
+        for tp in (1, 2, 3, 4):
+            ctx.set_launch("dd", threads, tp)
+            assert np.array_equal(ctx.evaluate_dd(p4).view(np.uint64), base.view(np.uint64))
+
+
+def test_dd_contract_under_cancellation(gpu):
+    """Adversarial inputs: duplicated monomials with opposite coefficients (exact cancellation
+    in every stage-3 sum), unit-modulus points (no decay along k = 16 product chains, d = 10),
+    and a wide dynamic range of coordinates."""
+    n, m, k, d = 24, 16, 16, 10
+    base = pj.random_system(n, m, k, d, 31)
+    s = pj.PolynomialSystem(n, m, k, d, base.positions.copy(), base.exponents.copy(), base.coeffs.copy())
+    for p in range(n):                      # monomial 2i+1 = monomial 2i with coefficient * -1
+        for g in range(0, m, 2):
+            a, b = p * m + g, p * m + g + 1
+            s.positions[b] = s.positions[a]
+            s.exponents[b] = s.exponents[a]
+            s.coeffs[b] = -s.coeffs[a]
+    S = sysd_of(s)
+    ctx = pj.EvaluationContext(s)
+    ang = np.random.default_rng(3).uniform(0, 2 * np.pi, (6, n))
+    unit = np.exp(1j * ang)
+    scale = 2.0 ** np.random.default_rng(4).integers(-12, 12, (6, n))
+    for pts in (unit, unit * scale):
+        p4 = stress_dd(pts, 5)
+        want, ms = O.evaluate("dd", S, p4, magsum=True)
+        got = ctx.evaluate_dd(p4)
+        assert dd_rel(got, want, ms) <= DD_TOL
+        # exact cancellation: every value and Jacobian entry is (near) zero relative to its terms
+        mag = np.abs(got[..., 0]) + np.abs(got[..., 2])
+        assert np.all(mag <= 1e-30 * np.maximum(ms, 1e-300) + (ms == 0))
+    # and a generic system on unit-modulus points (longest undamped chains)
+    s2 = pj.random_system(n, m, k, d, 32)
+    S2 = sysd_of(s2)
+    c2 = pj.EvaluationContext(s2)
+    p4 = stress_dd(unit, 6)
+    want, ms = O.evaluate("dd", S2, p4, magsum=True)
+    assert dd_rel(c2.evaluate_dd(p4), want, ms) <= DD_TOL
