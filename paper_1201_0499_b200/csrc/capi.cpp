@@ -241,7 +241,7 @@ int choose_launch(pj_ctx* c, int mode) {
             for (int tp : ftps) {
                 const size_t sm = smem_need_fast(c, nw, tp);
                 if (sm > c->smem_optin) continue;
-                consider(1, nw, tp, sm, pjb::fast_blocks_per_sm(c->k, c->n, nw * 32, sm));
+                consider(1, nw, tp, sm, pjb::fast_blocks_per_sm(c->k, c->n, c->d, nw * 32, sm));
             }
     }
     if (best_score < 0) {

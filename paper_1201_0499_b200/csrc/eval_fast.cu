@@ -77,8 +77,11 @@ __device__ __forceinline__ bool fin(const CDD& v) {
 
 // NS: compile-time plane stride of the shared-memory point tables (>= n), so that the four
 // component loads of a gather share one address register (immediate offsets).
-template <int K, int NS>
-__global__ void __launch_bounds__(256) fast_kernel(DevSystem S, const double* __restrict__ pts,
+#ifndef PJB_FAST_MINB
+#define PJB_FAST_MINB 2  // 2 CTAs x 256 threads: caps registers at 128 (measured best, tools/tune.py)
+#endif
+template <int K, int NS, bool D2>
+__global__ void __launch_bounds__(256, PJB_FAST_MINB) fast_kernel(DevSystem S, const double* __restrict__ pts,
                                                    double* __restrict__ out, long long B, int TP,
                                                    int* __restrict__ flag) {
     constexpr int W = 4;
@@ -111,7 +114,7 @@ __global__ void __launch_bounds__(256) fast_kernel(DevSystem S, const double* __
             st_pl(tab + t * tabPt + v, NS, x);
         }
         __syncthreads();
-        if (d > 2) {  // power chains, ref kernels.cpp:16-24 (normalised products: shared table)
+        if (!D2) {  // power chains, ref kernels.cpp:16-24 (normalised products: shared table)
             for (int i = threadIdx.x; i < tp * n; i += blockDim.x) {
                 const int t = i / n, v = i - t * n;
                 double* pb = tab + t * tabPt + v;
@@ -155,9 +158,15 @@ __global__ void __launch_bounds__(256) fast_kernel(DevSystem S, const double* __
                             __ldg(cf + (j * W + 3) * 32)};
                 };
                 auto X = [&](int j) -> CDD { return ld_pl(xt + pos[j], NS); };
+                // x^(a_j - 1): branch-free. d <= 2 (D2): select between 1 and the gathered x;
+                // otherwise a table load (row max(a_j - 2, 0)) and a select for a_j == 1
                 auto PWsel = [&](int j, const CDD& v) -> CDD {
-                    if (d <= 2) return sel_cdd(ex1[j] != 0, v, one);
-                    return ex1[j] == 0 ? one : ld_pl(xt + (ex1[j] - 1) * W * NS + pos[j], NS);
+                    if constexpr (D2) {
+                        return sel_cdd(ex1[j] != 0, v, one);
+                    } else {
+                        const int e = ex1[j] > 0 ? ex1[j] - 1 : 0;
+                        return sel_cdd(ex1[j] != 0, ld_pl(xt + e * W * NS + pos[j], NS), one);
+                    }
                 };
                 auto SLOT = [&](int j) -> double* { return stg + j * W * 32 + lane; };
 
@@ -263,10 +272,10 @@ __global__ void __launch_bounds__(256) fast_kernel(DevSystem S, const double* __
 // ----------------------------------------------------------------------------- dispatch
 namespace {
 
-template <int K, int NS>
+template <int K, int NS, bool D2>
 cudaError_t launch_t(const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
                      cudaStream_t st) {
-    auto kern = fast_kernel<K, NS>;
+    auto kern = fast_kernel<K, NS, D2>;
     if (L.smem_bytes > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem_bytes);
         if (e != cudaSuccess) return e;
@@ -275,27 +284,36 @@ cudaError_t launch_t(const LaunchCfg& L, const DevSystem& S, const double* pts, 
     return cudaGetLastError();
 }
 
-template <int K, int NS>
+template <int K, int NS, bool D2>
 int occ_t(int threads, size_t smem) {
-    auto kern = fast_kernel<K, NS>;
+    auto kern = fast_kernel<K, NS, D2>;
     if (smem > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
         return 0;
     int nb = 0;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem) == cudaSuccess ? nb : 0;
 }
 
+template <int K, bool D2>
+cudaError_t launch_kd(int ns, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
+                      cudaStream_t st) {
+    if (ns == 32) return launch_t<K, 32, D2>(L, S, pts, out, B, st);
+    if (ns == 64) return launch_t<K, 64, D2>(L, S, pts, out, B, st);
+    return launch_t<K, 256, D2>(L, S, pts, out, B, st);
+}
 template <int K>
 cudaError_t launch_k(int ns, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
                      cudaStream_t st) {
-    if (ns == 32) return launch_t<K, 32>(L, S, pts, out, B, st);
-    if (ns == 64) return launch_t<K, 64>(L, S, pts, out, B, st);
-    return launch_t<K, 256>(L, S, pts, out, B, st);
+    return S.d <= 2 ? launch_kd<K, true>(ns, L, S, pts, out, B, st) : launch_kd<K, false>(ns, L, S, pts, out, B, st);
+}
+template <int K, bool D2>
+int occ_kd(int ns, int threads, size_t smem) {
+    if (ns == 32) return occ_t<K, 32, D2>(threads, smem);
+    if (ns == 64) return occ_t<K, 64, D2>(threads, smem);
+    return occ_t<K, 256, D2>(threads, smem);
 }
 template <int K>
-int occ_k(int ns, int threads, size_t smem) {
-    if (ns == 32) return occ_t<K, 32>(threads, smem);
-    if (ns == 64) return occ_t<K, 64>(threads, smem);
-    return occ_t<K, 256>(threads, smem);
+int occ_k(int ns, int d, int threads, size_t smem) {
+    return d <= 2 ? occ_kd<K, true>(ns, threads, smem) : occ_kd<K, false>(ns, threads, smem);
 }
 
 }  // namespace
@@ -328,11 +346,11 @@ cudaError_t launch_fast(int k, const LaunchCfg& L, const DevSystem& S, const dou
     }
 }
 
-int fast_blocks_per_sm(int k, int n, int threads, size_t smem) {
+int fast_blocks_per_sm(int k, int n, int d, int threads, size_t smem) {
     const int ns = fast_plane_stride(n);
     switch (k) {
 #define PJB_CASE(KK) \
-    case KK: return occ_k<KK>(ns, threads, smem);
+    case KK: return occ_k<KK>(ns, d, threads, smem);
         PJB_FAST_KS(PJB_CASE)
 #undef PJB_CASE
         default: return 0;

@@ -59,6 +59,6 @@ bool fast_supported(int k);
 int fast_plane_stride(int n);
 cudaError_t launch_fast(int k, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
                         cudaStream_t st);
-int fast_blocks_per_sm(int k, int n, int threads, size_t smem);
+int fast_blocks_per_sm(int k, int n, int d, int threads, size_t smem);
 
 }  // namespace pjb
