@@ -10,7 +10,7 @@ import ctypes
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-SO_PATH = os.path.join(HERE, "libpolyjac_b200.so")
+SO_PATH = os.environ.get("PJ_LIB_PATH") or os.path.join(HERE, "libpolyjac_b200.so")  # override: experiments
 
 PJ_OK, PJ_EINVAL, PJ_ERANGE, PJ_ECUDA, PJ_ENOMEM, PJ_ENONFINITE = 0, 1, 2, 3, 4, 5
 PJ_PREC_D, PJ_PREC_DD = 1, 2

@@ -118,8 +118,10 @@ struct pj_ctx {
     int* d_gm_off = nullptr;
     uint16_t* d_gm_ent = nullptr;
     std::vector<uint32_t> sch, seg;  // fast-kernel stage-3 schedule (host copies)
+    std::vector<uint16_t> segcode;
     uint32_t* d_sch = nullptr;
     uint32_t* d_seg = nullptr;
+    uint16_t* d_segcode = nullptr;
     int nseg = 0;
     int* d_flag = nullptr;
     double* d_coef[2] = {};  // coefficient planes: [0] complex double, [1] complex dd
@@ -152,6 +154,7 @@ struct pj_ctx {
         S.sch = d_sch;
         S.seg = d_seg;
         S.nseg = nseg;
+        S.segcode = d_segcode;
         S.coefT = d_coefT;
         return S;
     }
@@ -173,6 +176,7 @@ void free_ctx(pj_ctx* c) {
     cudaFree(c->d_gm_ent);
     cudaFree(c->d_sch);
     cudaFree(c->d_seg);
+    cudaFree(c->d_segcode);
     cudaFree(c->d_flag);
     cudaFree(c->d_coef[0]);
     cudaFree(c->d_coef[1]);
@@ -202,7 +206,7 @@ size_t smem_need_fast(const pj_ctx* c, int nw, int tp) {
     const size_t D1 = c->d > 2 ? c->d - 1 : 1;
     const size_t tab = D1 * 4 * size_t(pjb::fast_plane_stride(c->n));
     const size_t acc = c->chunks > 1 ? size_t(c->n + 1) * 4 : 0;
-    const size_t per_warp = size_t(c->k + 1) * 4 * 32 + size_t(c->nseg) * 4 + acc;
+    const size_t per_warp = size_t(c->k + 1) * 4 * 32 + acc;
     return (tp * tab + nw * per_warp) * sizeof(double);
 }
 
@@ -215,12 +219,11 @@ int choose_launch(pj_ctx* c, int mode) {
     std::vector<int> nws = {8, 4, 2, 1}, tps = {8, 4, 2, 1};
     if (M.over_threads) nws = {M.over_threads / 32};
     if (M.over_tp) tps = {M.over_tp};
-    auto consider = [&](int variant, int nw, int tp, size_t sm, int nb) {
+    auto consider = [&](int variant, int nw, int tp, size_t sm, int nb, int bonus) {
         if (nb <= 0) return;
-        // resident warps first; then fewer, fatter tiles (more coefficient reuse) as long as
-        // a tile still has a task per warp
+        // resident warps first, then the tile-size preference (bonus)
         const int warps = std::min(nb * nw, 64);
-        const int score = warps * 64 + (tp * c->n >= nw ? tp : 0);
+        const int score = warps * 64 + bonus;
         if (score > best_score) {
             best_score = score;
             best.variant = variant;
@@ -235,13 +238,16 @@ int choose_launch(pj_ctx* c, int mode) {
         // smaller tiles measured faster for the fast kernel (finer grid-stride balance)
         // measured (tools/tune.py): 8-warp CTAs beat more, smaller CTAs at equal residency;
         // among tiles that keep the residency, the largest (<= 4) is marginally best
-        std::vector<int> ftps = M.over_tp ? tps : std::vector<int>{4, 2, 1};
+        // measured (tools/tune.py): 8-warp CTAs beat more, smaller CTAs at equal residency;
+        // at equal residency 2-point tiles are best (C1: 0.853 vs 0.851 (1); C3: 0.763 vs 0.72 (4))
+        std::vector<int> ftps = M.over_tp ? tps : std::vector<int>{2, 4, 1};
         std::vector<int> fnws = M.over_threads ? nws : std::vector<int>{8};
         for (int nw : fnws)
-            for (int tp : ftps) {
+            for (size_t i = 0; i < ftps.size(); ++i) {
+                const int tp = ftps[i];
                 const size_t sm = smem_need_fast(c, nw, tp);
                 if (sm > c->smem_optin) continue;
-                consider(1, nw, tp, sm, pjb::fast_blocks_per_sm(c->k, c->n, c->d, nw * 32, sm));
+                consider(1, nw, tp, sm, pjb::fast_blocks_per_sm(c->k, c->n, c->d, nw * 32, sm), int(ftps.size() - i));
             }
     }
     if (best_score < 0) {
@@ -249,7 +255,8 @@ int choose_launch(pj_ctx* c, int mode) {
             for (int tp : tps) {
                 const size_t sm = smem_need(c, W, nw, tp);
                 if (sm > c->smem_optin) continue;
-                consider(-1, nw, tp, sm, pjb::max_blocks_per_sm(precflag, 0, nw * 32, sm));
+                // fewer, fatter tiles (coefficient reuse) as long as a tile has a task per warp
+                consider(-1, nw, tp, sm, pjb::max_blocks_per_sm(precflag, 0, nw * 32, sm), tp * c->n >= nw ? tp : 0);
             }
     }
     if (best_score < 0) {
@@ -393,6 +400,7 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
         c->nseg = n + 1 + 32;
         c->sch.assign(size_t(n) * C * R * 32, 0);
         c->seg.assign(size_t(n) * C * (n + 1), 0);
+        c->segcode.assign(size_t(n) * C * c->nseg, 0);
         std::vector<std::pair<int, uint32_t>> ent;  // (output, staging code)
         for (int p = 0; p < n; ++p)
             for (int ch = 0; ch < C; ++ch) {
@@ -419,6 +427,7 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
                         }
                         prev_o = o;
                         const bool flush = q + 1 == b || ent[q + 1].first != o;
+                        if (flush) c->segcode[(size_t(p) * C + ch) * c->nseg + segid] = uint16_t(ent[q].second);
                         sc[size_t(q - a) * 32 + lane] =
                             ent[q].second | (uint32_t(segid) << 13) | (flush ? pjb::kSchFlush : 0) | pjb::kSchValid;
                     }
@@ -454,6 +463,7 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
         (e = up((void**)&c->d_gm_ent, c->gm_ent.data(), c->gm_ent.size() * 2)) ||
         (e = up((void**)&c->d_sch, c->sch.data(), c->sch.size() * 4)) ||
         (e = up((void**)&c->d_seg, c->seg.data(), c->seg.size() * 4)) ||
+        (e = up((void**)&c->d_segcode, c->segcode.data(), c->segcode.size() * 2)) ||
         (e = cudaMalloc((void**)&c->d_flag, sizeof(int))) || (e = cudaMemset(c->d_flag, 0, sizeof(int)))) {
         free_ctx(c);
         cudaSetDevice(prev);

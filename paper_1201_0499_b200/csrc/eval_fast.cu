@@ -77,11 +77,14 @@ __device__ __forceinline__ bool fin(const CDD& v) {
 
 // NS: compile-time plane stride of the shared-memory point tables (>= n), so that the four
 // component loads of a gather share one address register (immediate offsets).
-#ifndef PJB_FAST_MINB
-#define PJB_FAST_MINB 2  // 2 CTAs x 256 threads: caps registers at 128 (measured best, tools/tune.py)
-#endif
+// Register budget: 3 CTAs x 256 threads (<= 85 registers) for k <= 12, where the per-warp
+// staging also fits three CTAs; 2 CTAs (<= 128 registers) above. Measured with tools/tune.py:
+// k = 8: 0.853 (3 CTAs) vs 0.843 (2 CTAs); k = 16: 0.763 (2 CTAs) vs 0.723 (3 CTAs).
+template <int K>
+constexpr int fast_min_blocks() { return K <= 12 ? 3 : 2; }
+
 template <int K, int NS, bool D2>
-__global__ void __launch_bounds__(256, PJB_FAST_MINB) fast_kernel(DevSystem S, const double* __restrict__ pts,
+__global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSystem S, const double* __restrict__ pts,
                                                    double* __restrict__ out, long long B, int TP,
                                                    int* __restrict__ flag) {
     constexpr int W = 4;
@@ -92,13 +95,10 @@ __global__ void __launch_bounds__(256, PJB_FAST_MINB) fast_kernel(DevSystem S, c
     const int n = S.n, m = S.m, d = S.d, C = S.chunks;
     const int D1 = d > 2 ? d - 1 : 1;
     const int tabPt = D1 * W * NS;
-    const int NSEG = S.nseg;
-    const int segW = NSEG * W;
     const int accW = C > 1 ? (n + 1) * W : 0;
     double* tab = smem_;
-    double* stg = smem_ + TP * tabPt + warp * (stgW + segW + accW);
-    double* seg = stg + stgW;
-    double* acc = seg + segW;
+    double* stg = smem_ + TP * tabPt + warp * (stgW + accW);
+    double* acc = stg + stgW;
     const long long ntiles = (B + TP - 1) / TP;
     const long long nout = (long long)n * n + n;
     const CDD one = {1.0, 0.0, 0.0, 0.0};
@@ -231,8 +231,9 @@ __global__ void __launch_bounds__(256, PJB_FAST_MINB) fast_kernel(DevSystem S, c
                             lr = __dadd_rn(lr, __dadd_rn(tv.rl, a.lo));
                             li = __dadd_rn(li, __dadd_rn(tv.il, b.lo));
                             if (code & kSchFlush) {
-                                const int sg = (code >> 13) & 0x3ff;
-                                st_pl(seg + sg, NSEG, CDD{sr, lr, si, li});
+                                // the partial overwrites the staging slot this lane just consumed
+                                // (each slot is read exactly once, by this lane): no extra smem
+                                st_pl(stg + (ent >> 5) * W * 32 + (ent & 31), 32, CDD{sr, lr, si, li});
                                 sr = lr = si = li = 0.0;
                             }
                         }
@@ -249,9 +250,16 @@ __global__ void __launch_bounds__(256, PJB_FAST_MINB) fast_kernel(DevSystem S, c
                     const uint32_t sd = __ldg(S.seg + (size_t)(p * C + c) * (n + 1) + o);
                     const int first = sd & 0xffff, cnt = sd >> 16;
                     CDD r = c == 0 ? zero : ld_pl(acc + o, n + 1);
-                    for (int qq = 0; qq < cnt; ++qq) {
-                        const CDD sv = ld_pl(seg + first + qq, NSEG);
-                        r = (c == 0 && qq == 0) ? sv : cdd_add(r, sv);
+                    const uint16_t* sgc = S.segcode + (size_t)(p * C + c) * S.nseg + first;
+                    int qq = 0;
+                    if (c == 0 && cnt > 0) {
+                        const int e = __ldg(sgc);
+                        r = ld_pl(stg + (e >> 5) * W * 32 + (e & 31), 32);
+                        qq = 1;
+                    }
+                    for (; qq < cnt; ++qq) {
+                        const int e = __ldg(sgc + qq);
+                        r = cdd_add(r, ld_pl(stg + (e >> 5) * W * 32 + (e & 31), 32));
                     }
                     if (last) {
                         if (t < tp) {
