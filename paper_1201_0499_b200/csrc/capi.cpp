@@ -358,14 +358,15 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
             }
         }
     }
-    // the same dd coefficients tiled per (row, 32-monomial chunk), lane index fastest
-    std::vector<double> cddT(size_t(c->n) * c->chunks * (k + 1) * 4 * 32, 0.0);
+    // the fast kernel seeds its backward chain with the plain coefficient c and applies the
+    // power rule as an exact scaling, so it needs only c: dd, tiled per (row, 32-monomial chunk),
+    // lane index fastest
+    std::vector<double> cddT(size_t(c->n) * c->chunks * 4 * 32, 0.0);
     for (int p = 0; p < c->n; ++p)
         for (int g = 0; g < c->m; ++g) {
             const size_t s = size_t(p) * c->m + g;
-            const size_t base = (size_t(p) * c->chunks + g / 32) * (k + 1) * 4 * 32 + (g & 31);
-            for (size_t j = 0; j <= k; ++j)
-                for (int q = 0; q < 4; ++q) cddT[base + (j * 4 + q) * 32] = cdd[(j * 4 + q) * nm + s];
+            const size_t base = (size_t(p) * c->chunks + g / 32) * 4 * 32 + (g & 31);
+            for (int q = 0; q < 4; ++q) cddT[base + q * 32] = sys->coeffs[4 * s + q];
         }
     // stage-3 gather map: for (row p, chunk c, column v) the ascending-g list of (g, j) with
     // positions[s*k+j] == v — the inverse of the reference's derivative slot map

@@ -134,38 +134,58 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
                 const int graw = c * 32 + lane;
                 const int g = graw < m ? graw : m - 1;  // inactive lanes shadow a real monomial
                 const int s = p * m + g;
-                int pos[K], ex1[K];
+                // fused position/exponent words, kept packed (K/2 registers) and decoded on use:
+                // the exponents are needed again at the end of the backward chain
+                uint32_t pw[(K + 7) / 8 * 4];
                 {
                     const uint4* row = reinterpret_cast<const uint4*>(S.posexp + (size_t)s * S.kp);
 #pragma unroll
                     for (int q = 0; q < (K + 7) / 8; ++q) {
                         const uint4 w = __ldg(row + q);
-                        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-                        for (int h = 0; h < 8; ++h) {
-                            if (q * 8 + h < K) {
-                                const uint32_t u = (ws[h >> 1] >> ((h & 1) * 16)) & 0xffffu;
-                                pos[q * 8 + h] = u & 255;
-                                ex1[q * 8 + h] = u >> 8;
-                            }
-                        }
+                        pw[4 * q + 0] = w.x;
+                        pw[4 * q + 1] = w.y;
+                        pw[4 * q + 2] = w.z;
+                        pw[4 * q + 3] = w.w;
                     }
                 }
-                // coefficients of this (row, chunk), lane-minor tiles: immediate offsets per (j, comp)
-                const double* cf = S.coefT + (size_t)(p * C + c) * (K + 1) * W * 32 + lane;
-                auto COEF = [&](int j) -> CDD {
-                    return {__ldg(cf + (j * W + 0) * 32), __ldg(cf + (j * W + 1) * 32), __ldg(cf + (j * W + 2) * 32),
-                            __ldg(cf + (j * W + 3) * 32)};
+                auto POS = [&](int j) -> int { return (pw[j >> 1] >> ((j & 1) * 16)) & 255u; };
+                auto EX1 = [&](int j) -> int { return (pw[j >> 1] >> ((j & 1) * 16 + 8)) & 255u; };
+                // prefetch the stage-3 schedule of this (row, chunk) into registers now, so its L2
+                // latency hides behind stage 2 (in-order issue would otherwise stall on it)
+                const size_t pc = (size_t)(p * C + c);
+                uint32_t codes[R];
+                {
+                    const uint32_t* sc = S.sch + pc * R * 32 + lane;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) codes[r] = __ldg(sc + r * 32);
+                }
+                const uint32_t sd0 = lane <= n ? __ldg(S.seg + pc * (n + 1) + lane) : 0u;
+                const int seg0 = lane <= n && (sd0 >> 16) > 0 ? __ldg(S.segcode + pc * S.nseg + (sd0 & 0xffff)) : 0;
+                // the monomial's coefficient c (lane-minor tile of this (row, chunk))
+                const double* cf = S.coefT + pc * W * 32 + lane;
+                // power-rule scaling a_j * x: d <= 2 means a_j in {1, 2}, an exact scaling of every
+                // word; otherwise TwoProd of the high word by the small integer, low word folded in
+                auto SCALE = [&](int j, const CDD& x) -> CDD {
+                    if constexpr (D2) {
+                        const double a = EX1(j) ? 2.0 : 1.0;
+                        return {__dmul_rn(x.rh, a), __dmul_rn(x.rl, a), __dmul_rn(x.ih, a), __dmul_rn(x.il, a)};
+                    } else {
+                        const double a = (double)(EX1(j) + 1);
+                        const double pr = __dmul_rn(x.rh, a), pi = __dmul_rn(x.ih, a);
+                        return {pr, __fma_rn(x.rl, a, __fma_rn(x.rh, a, -pr)), pi,
+                                __fma_rn(x.il, a, __fma_rn(x.ih, a, -pi))};
+                    }
                 };
-                auto X = [&](int j) -> CDD { return ld_pl(xt + pos[j], NS); };
+                auto X = [&](int j) -> CDD { return ld_pl(xt + POS(j), NS); };
                 // x^(a_j - 1): branch-free. d <= 2 (D2): select between 1 and the gathered x;
                 // otherwise a table load (row max(a_j - 2, 0)) and a select for a_j == 1
                 auto PWsel = [&](int j, const CDD& v) -> CDD {
                     if constexpr (D2) {
-                        return sel_cdd(ex1[j] != 0, v, one);
+                        return sel_cdd(EX1(j) != 0, v, one);
                     } else {
-                        const int e = ex1[j] > 0 ? ex1[j] - 1 : 0;
-                        return sel_cdd(ex1[j] != 0, ld_pl(xt + e * W * NS + pos[j], NS), one);
+                        const int e1 = EX1(j);
+                        const int e = e1 > 0 ? e1 - 1 : 0;
+                        return sel_cdd(e1 != 0, ld_pl(xt + e * W * NS + POS(j), NS), one);
                     }
                 };
                 auto SLOT = [&](int j) -> double* { return stg + j * W * 32 + lane; };
@@ -191,24 +211,32 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
                         vlast = v;
                     }
                 }
-                // ---- stage 2, back-fused: q = f; L'_j = F_j * q; q *= v_j
+                // ---- stage 2, back-fused and coefficient-seeded: q = f * c; L'_j = F_j * q;
+                // q *= v_j. Every staged derivative then already carries c, and the power rule
+                // is the cheap exact scaling a_j * L'_j (ref kernels.cpp:108-118 multiplies by the
+                // pre-scaled a_j * c instead: k + 1 complex products, here 1 product + k scalings)
                 constexpr bool f_norm = ((K - 1) & 1) == 0;
                 CDD q;
                 {
-                    const CDD L = cdd_mul_u(Fc, f);
-                    st_pl(SLOT(K - 1), 32, cdd_mul_u(L, COEF(K - 1)));
-                    st_pl(SLOT(K), 32, cdd_mul_u(cdd_mul(L, vlast), COEF(K)));
-                    q = cmul_n(!f_norm, f, vlast);
+                    const CDD cval = {__ldg(cf), __ldg(cf + 32), __ldg(cf + 64), __ldg(cf + 96)};
+                    const CDD q0 = cmul_n(!f_norm, f, cval);  // normalised iff f was not
+                    const CDD L = cdd_mul_u(Fc, q0);
+                    st_pl(SLOT(K - 1), 32, SCALE(K - 1, L));
+                    st_pl(SLOT(K), 32, cdd_mul(L, vlast));
+                    q = cmul_n(f_norm, q0, vlast);
                 }
 #pragma unroll
                 for (int j = K - 2; j >= 1; --j) {
-                    const bool q_norm = (((K - 2 - j) & 1) == 0) ? !f_norm : f_norm;  // state of q here
+                    const bool q_norm = (((K - 2 - j) & 1) == 0) ? f_norm : !f_norm;  // state of q here
                     const CDD L = cdd_mul_u(ld_pl(SLOT(j), 32), q);
-                    st_pl(SLOT(j), 32, cdd_mul_u(L, COEF(j)));
+                    st_pl(SLOT(j), 32, SCALE(j, L));
                     q = cmul_n(!q_norm, q, X(j));
                 }
-                st_pl(SLOT(0), 32, cdd_mul_u(q, COEF(0)));
+                st_pl(SLOT(0), 32, SCALE(0, q));
                 __syncwarp();
+#ifdef PJB_EXP_NO_STAGE3
+                if (codes[0] != 0xdeadbeefu) continue;  // experiment: stage 2 only
+#endif
                 // ---- stage 3, phase 1: balanced segmented sums. The (row, chunk) schedule
                 // hands every lane R consecutive entries of the output-major, ascending-g list
                 // of staged terms; a lane flushes its running sum at segment ends. The running
@@ -217,14 +245,14 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
                 // is one dependent add per term); the partial is renormalised by the phase-2 add.
                 // Error <= ~(c^3/6 + 3c) u^2 * sum|terms| for a segment of c <= k+1 terms.
                 {
-                    const uint32_t* sc = S.sch + (size_t)(p * C + c) * R * 32 + lane;
                     double sr = 0.0, lr = 0.0, si = 0.0, li = 0.0;
 #pragma unroll
                     for (int r = 0; r < R; ++r) {
-                        const uint32_t code = __ldg(sc + r * 32);
+                        const uint32_t code = codes[r];
                         if (code & kSchValid) {
                             const int ent = code & 0x1fff;
-                            const CDD tv = ld_pl(stg + (ent >> 5) * W * 32 + (ent & 31), 32);
+                            double* sl = stg + (ent >> 5) * W * 32 + (ent & 31);
+                            const CDD tv = ld_pl(sl, 32);
                             const DD a = two_sum(sr, tv.rh), b = two_sum(si, tv.ih);
                             sr = a.hi;
                             si = b.hi;
@@ -233,7 +261,7 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
                             if (code & kSchFlush) {
                                 // the partial overwrites the staging slot this lane just consumed
                                 // (each slot is read exactly once, by this lane): no extra smem
-                                st_pl(stg + (ent >> 5) * W * 32 + (ent & 31), 32, CDD{sr, lr, si, li});
+                                st_pl(sl, 32, CDD{sr, lr, si, li});
                                 sr = lr = si = li = 0.0;
                             }
                         }
@@ -247,14 +275,15 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
                 for (int k2 = 0; k2 * 32 <= n; ++k2) {
                     const int o = k2 == 0 ? lane : 32 * k2 + (31 - lane);
                     if (o > n) continue;
-                    const uint32_t sd = __ldg(S.seg + (size_t)(p * C + c) * (n + 1) + o);
+                    const uint32_t sd = k2 == 0 ? sd0 : __ldg(S.seg + pc * (n + 1) + o);
                     const int first = sd & 0xffff, cnt = sd >> 16;
                     CDD r = c == 0 ? zero : ld_pl(acc + o, n + 1);
-                    const uint16_t* sgc = S.segcode + (size_t)(p * C + c) * S.nseg + first;
+                    const uint16_t* sgc = S.segcode + pc * S.nseg + first;
                     int qq = 0;
-                    if (c == 0 && cnt > 0) {
-                        const int e = __ldg(sgc);
-                        r = ld_pl(stg + (e >> 5) * W * 32 + (e & 31), 32);
+                    if (cnt > 0) {
+                        const int e = k2 == 0 ? seg0 : __ldg(sgc);
+                        const CDD sv = ld_pl(stg + (e >> 5) * W * 32 + (e & 31), 32);
+                        r = c == 0 ? sv : cdd_add(r, sv);
                         qq = 1;
                     }
                     for (; qq < cnt; ++qq) {

@@ -35,8 +35,8 @@ struct DevSystem {
     // staging code (j*32 + g) of the last entry of every segment, per (p, c): phase 1 leaves the
     // segment's partial in that staging slot
     const uint16_t* segcode;
-    // dd coefficients tiled for the fast kernel: component c of (j, g = 32*chunk + lane) of row
-    // p at coefT[((p*chunks + chunk)*(k+1)*4 + j*4 + c)*32 + lane] (zero for g >= m)
+    // plain dd coefficients tiled for the fast kernel: component q of monomial
+    // g = 32*chunk + lane of row p at coefT[((p*chunks + chunk)*4 + q)*32 + lane] (0 for g >= m)
     const double* coefT;
 };
 constexpr uint32_t kSchFlush = 1u << 23;
