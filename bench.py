@@ -303,11 +303,13 @@ def main():
     achieved = flops * B / (kern_ms * 1e-3) / 1e12
     io_bytes = B * (N * 32 + nout * 32)
     traffic = None
+    ncu = {}
     prof = os.path.join(ROOT, "profiles", "ncu_summary.json")
     if os.path.exists(prof):
         try:
             with open(prof) as fh:
-                traffic = json.load(fh).get("dram_bytes_per_launch")
+                ncu = json.load(fh)
+            traffic = ncu.get("dram_bytes_per_launch")
         except (OSError, ValueError):
             traffic = None
     roofline = {"bound": "fp64", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
@@ -315,7 +317,25 @@ def main():
                 "hbm_gbs_achieved": io_bytes / (kern_ms * 1e-3) / 1e9,
                 "flops_per_eval": flops,
                 "peak_source": "pj_fp64_peak_probe: DFMA throughput measured live on this device (2 flops/DFMA); "
-                               "MEASURED_PEAKS.json carries no FP64 figure"}
+                               "MEASURED_PEAKS.json carries no FP64 figure",
+                "note": "achieved = the fixed SURVEY.md 8(d) cost model (80 flops per complex dd product, 40 per "
+                        "add) over device time; the kernel executes fewer FP64 instructions than the model "
+                        "counts (coefficient-seeded back-fused products, 32-38 instead of 68 instructions per "
+                        "product) - the instruction-level view is in ncu_* (committed capture)"}
+    if ncu.get("launches"):
+        L0 = ncu["launches"][0]
+        roofline["ncu_kernel"] = ncu.get("kernel")
+        roofline["ncu_fp64_pipe_active_pct"] = L0.get("fp64_pipe_active_pct")
+        roofline["ncu_issue_active_pct"] = L0.get("issue_active_pct")
+    hw = os.path.join(ROOT, "profiles", "fp64_exec.json")
+    if os.path.exists(hw):
+        try:
+            with open(hw) as fh:
+                h = json.load(fh)
+            roofline["ncu_hw_fp64_tflops"] = h.get("hw_fp64_tflops")
+            roofline["ncu_fp64_instr_per_eval"] = h.get("fp64_instr_per_eval")
+        except (OSError, ValueError):
+            pass
 
     line = {
         "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws, "steps": args.steps,
