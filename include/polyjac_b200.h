@@ -36,6 +36,7 @@ extern "C" {
 #define PJ_ENOMEM 4     /* device allocation failed */
 #define PJ_ENONFINITE 5 /* non-finite coordinate: std::invalid_argument in
                            ref src/engine.cpp:186-188 */
+#define PJ_EFORMAT 6    /* malformed system file: polyjac::FormatError, ref include/polyjac/io.hpp:19-21 */
 
 /* precision / order flags for pj_evaluate */
 #define PJ_PREC_D 1         /* complex double, reference operation order: bit-exact with
@@ -112,6 +113,20 @@ int pj_random_points(int n, int64_t count, uint64_t seed, double* points);
 /* Points [first, first + count) of the same stream (a contiguous shard of random_points(n, N,
  * seed) for any N >= first + count): lets each rank generate only its own shard. */
 int pj_random_points_range(int n, int64_t first, int64_t count, uint64_t seed, double* points);
+
+/* System text files (ref src/io.cpp:38-117, format ref README.md:91-104): '#' comments, header
+ * "n m k d", one "re im pos1 exp1 ... posk expk" line per monomial (1-based positions), doubles
+ * with 17 significant digits (bit-exact round trip). Errors: PJ_EFORMAT with "<name>:<line>: ..."
+ * in pj_last_error(), the reference's FormatError wording. A pj_system owns its arrays;
+ * pj_system_view exposes them as a descriptor for pj_ctx_create. */
+typedef struct pj_system pj_system;
+int pj_system_read_file(const char* path, pj_system** out);
+int pj_system_read_text(const char* text, const char* name, pj_system** out);
+int pj_system_view(const pj_system* sys, pj_system_desc* desc);
+void pj_system_free(pj_system* sys);
+int pj_system_write_file(const pj_system_desc* sys, const char* path);
+/* Writes the text into buf (capacity cap, NUL-terminated, may be NULL); returns its full length. */
+int64_t pj_system_write_text(const pj_system_desc* sys, char* buf, int64_t cap);
 
 /* Advanced: override the launch shape for `flags`' precision (threads per CTA, multiple of 32,
  * <= 256; points per CTA tile). 0 restores the automatic choice. */

@@ -94,6 +94,10 @@ def ref():
                                                         ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                                         ctypes.POINTER(ctypes.c_ulonglong), ctypes.POINTER(ctypes.c_double)]
         L.ref_naive.argtypes = [ctypes.c_int] * 4 + [_i32p, _i32p, _f64p, _f64p, _f64p]
+        L.ref_write_system.argtypes = [ctypes.c_int] * 4 + [_i32p, _i32p, _f64p, ctypes.c_char_p, ctypes.c_longlong]
+        L.ref_write_system.restype = ctypes.c_longlong
+        L.ref_read_system.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int), ctypes.c_void_p,
+                                      ctypes.c_void_p, ctypes.c_void_p, ctypes.c_longlong]
         _ref = L
     return _ref
 
@@ -232,3 +236,24 @@ def ref_validate(sysd, nterms=None):
 
 def ref_mons_slot(s, kind, var, n, m):
     return ref().ref_mons_slot(s, 0 if kind == "value" else 1, var, n, m)
+
+
+def ref_write_system(sysd):
+    n, m, k, d = sysd["n"], sysd["m"], sysd["k"], sysd["d"]
+    ln = ref().ref_write_system(n, m, k, d, sysd["pos"], sysd["exps"], sysd["coeffs"], None, 0)
+    buf = ctypes.create_string_buffer(ln + 1)
+    ref().ref_write_system(n, m, k, d, sysd["pos"], sysd["exps"], sysd["coeffs"], buf, ln + 1)
+    return buf.value.decode()
+
+
+def ref_read_system(text):
+    """Reference read_system on a string; raises RefError (FormatError text) on bad input."""
+    dims = (ctypes.c_int * 4)()
+    if ref().ref_read_system(text.encode(), dims, None, None, None, 0):
+        raise _ref_err()
+    n, m, k, d = list(dims)
+    pos = np.empty(n * m * k, np.int32)
+    exps = np.empty(n * m * k, np.int32)
+    coeffs = np.empty((n * m, 4), np.float64)
+    ref().ref_read_system(text.encode(), dims, pos.ctypes.data, exps.ctypes.data, coeffs.ctypes.data, n * m)
+    return dict(n=n, m=m, k=k, d=d, pos=pos, exps=exps, coeffs=coeffs)

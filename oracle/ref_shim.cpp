@@ -17,7 +17,10 @@
 #include <thread>
 #include <vector>
 
+#include <sstream>
+
 #include "polyjac/engine.hpp"
+#include "polyjac/io.hpp"
 #include "polyjac/oracle.hpp"
 #include "polyjac/packing.hpp"
 #include "polyjac/system.hpp"
@@ -238,6 +241,48 @@ int ref_naive(int n, int m, int k, int d, const int* pos, const int* exps, const
         for (size_t i = 0; i < j.size(); ++i) {
             out[2 * (n + i)] = j[i].re;
             out[2 * (n + i) + 1] = j[i].im;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return 1;
+    }
+}
+
+// reference write_system into buf (capacity cap); returns the text length
+long long ref_write_system(int n, int m, int k, int d, const int* pos, const int* exps, const double* coeffs,
+                           char* buf, long long cap) {
+    std::ostringstream os;
+    write_system(make_system(n, m, k, d, pos, exps, coeffs), os);
+    const std::string t = os.str();
+    if (buf && cap > 0) {
+        const size_t nb = std::min<size_t>(size_t(cap) - 1, t.size());
+        std::memcpy(buf, t.data(), nb);
+        buf[nb] = 0;
+    }
+    return (long long)t.size();
+}
+
+// reference read_system from text: 0 ok (arrays sized by the caller from the header), 1 on
+// FormatError (message in ref_last_error). dims[4] receives n m k d.
+int ref_read_system(const char* text, int* dims, int* pos, int* exps, double* coeffs, long long cap_terms) {
+    try {
+        std::istringstream is(text);
+        PolynomialSystem sys = read_system(is, "<test>");
+        dims[0] = sys.n;
+        dims[1] = sys.m;
+        dims[2] = sys.k;
+        dims[3] = sys.d;
+        if ((long long)sys.terms.size() > cap_terms) return 0;
+        for (size_t s = 0; s < sys.terms.size(); ++s) {
+            for (int j = 0; j < sys.k; ++j) {
+                pos[s * sys.k + j] = sys.terms[s].support.positions[j];
+                exps[s * sys.k + j] = sys.terms[s].support.exponents[j];
+            }
+            coeffs[4 * s] = sys.terms[s].coeff.re;
+            coeffs[4 * s + 1] = 0.0;
+            coeffs[4 * s + 2] = sys.terms[s].coeff.im;
+            coeffs[4 * s + 3] = 0.0;
         }
         return 0;
     } catch (const std::exception& e) {

@@ -12,7 +12,7 @@ import os
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.environ.get("PJ_LIB_PATH") or os.path.join(HERE, "libpolyjac_b200.so")  # override: experiments
 
-PJ_OK, PJ_EINVAL, PJ_ERANGE, PJ_ECUDA, PJ_ENOMEM, PJ_ENONFINITE = 0, 1, 2, 3, 4, 5
+PJ_OK, PJ_EINVAL, PJ_ERANGE, PJ_ECUDA, PJ_ENOMEM, PJ_ENONFINITE, PJ_EFORMAT = 0, 1, 2, 3, 4, 5, 6
 PJ_PREC_D, PJ_PREC_DD = 1, 2
 PJ_ORDER_REF, PJ_ORDER_FAST = 0x10, 0x20
 
@@ -21,6 +21,8 @@ EXPORTS = [
     "pj_evaluate_host", "pj_nonfinite_seen", "pj_layout_info", "pj_mons_slot", "pj_slot_targets",
     "pj_zero_mask", "pj_mult_counts", "pj_random_system", "pj_random_points", "pj_set_launch",
     "pj_get_launch", "pj_fp64_peak_probe", "pj_random_points_range", "pj_set_kernel_variant",
+    "pj_system_read_file", "pj_system_read_text", "pj_system_view", "pj_system_free", "pj_system_write_file",
+    "pj_system_write_text",
 ]
 
 
@@ -31,6 +33,10 @@ class SystemDesc(ctypes.Structure):
 
 class PolyjacError(RuntimeError):
     """CUDA / internal failure of the native library (PJ_ECUDA, PJ_ENOMEM)."""
+
+
+class FormatError(RuntimeError):
+    """Malformed system file (PJ_EFORMAT): polyjac::FormatError, ref include/polyjac/io.hpp:19-21."""
 
 
 _lib = None
@@ -67,6 +73,14 @@ def lib():
     L.pj_set_launch.argtypes = [vp, ctypes.c_int, ctypes.c_int, ctypes.c_int]
     L.pj_get_launch.argtypes = [vp, ctypes.c_int, i32p, i32p, i32p, i64p, i32p]
     L.pj_set_kernel_variant.argtypes = [vp, ctypes.c_int, ctypes.c_int]
+    L.pj_system_read_file.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
+    L.pj_system_read_text.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(vp)]
+    L.pj_system_view.argtypes = [vp, ctypes.POINTER(SystemDesc)]
+    L.pj_system_free.argtypes = [vp]
+    L.pj_system_free.restype = None
+    L.pj_system_write_file.argtypes = [ctypes.POINTER(SystemDesc), ctypes.c_char_p]
+    L.pj_system_write_text.argtypes = [ctypes.POINTER(SystemDesc), ctypes.c_char_p, i64]
+    L.pj_system_write_text.restype = i64
     L.pj_fp64_peak_probe.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     for name in EXPORTS:
         getattr(L, name)  # fail loudly on a stale library
@@ -89,4 +103,6 @@ def check(rc: int, what: str = "") -> None:
         raise IndexError(msg)          # std::out_of_range
     if rc == PJ_ENOMEM:
         raise MemoryError(msg)
+    if rc == PJ_EFORMAT:
+        raise FormatError(msg)
     raise PolyjacError(msg)

@@ -15,11 +15,12 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 SO = os.path.join(HERE, "libpolyjac_b200.so")
+CLI = os.path.join(HERE, "polyjac_b200")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 CU = ["eval_kernels.cu", "eval_fast.cu", "fp64_probe.cu"]
-CPP = ["capi.cpp"]
+CPP = ["capi.cpp", "sysio.cpp"]
 HEADERS = ["dd.cuh", "eval_kernels.h"]
 
 
@@ -71,6 +72,13 @@ def build(force: bool = False, verbose: bool = False) -> str:
         fh.write("{ global: pj_*; local: *; };\n")
     if force or _newer(SO, objs):
         _run([NVCC, *ARCH, "-shared", "-o", SO, *objs, "-Xlinker", "--version-script=" + vs])
+    # command-line front end (f3): links the library with an $ORIGIN rpath
+    cli_src = os.path.join(CSRC, "cli.cpp")
+    cli_obj = os.path.join(BUILD, "cli.cpp.o")
+    if force or _newer(cli_obj, [cli_src] + hdrs):
+        _run(["g++", "-std=c++17", "-O2", "-I/usr/local/cuda/include", "-c", cli_src, "-o", cli_obj])
+    if force or _newer(CLI, [cli_obj, SO]):
+        _run([NVCC, *ARCH, "-o", CLI, cli_obj, "-L" + HERE, "-lpolyjac_b200", "-Xlinker", "-rpath,$ORIGIN"])
     return SO
 
 

@@ -19,6 +19,13 @@
 namespace {
 
 thread_local std::string g_err;
+}  // namespace
+
+namespace pjb {
+void set_last_error(const std::string& msg) { g_err = msg; }
+}  // namespace pjb
+
+namespace {
 
 int fail(int code, const std::string& msg) {
     g_err = msg;

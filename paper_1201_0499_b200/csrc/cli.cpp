@@ -1,0 +1,343 @@
+// polyjac_b200 — command-line front end over the C ABI, with the
+// reference CLI's subcommands, flags, exit codes (0 ok, 1 correctness failure, 2 usage or
+// file-format error) and machine-readable RESULT line (ref tools/main.cpp:36-228):
+//
+//   polyjac_b200 generate --n N --m M --k K --d D [--seed S] --out PATH
+//   polyjac_b200 bench (--system PATH | --n N --m M --k K --d D) [--seed S] [--evals E]
+//                      [--points B] [--precision dd|d] [--device G]
+//   polyjac_b200 check --system PATH [--points P] [--seed S] [--tol T] [--device G]
+//
+// The correctness gate compares the two device arithmetic paths with each other: the complex
+// double path (bit-exact with the reference's EvaluationContext::evaluate) and the complex
+// double-double path, per entry in the reference's relative-error convention
+// (ref src/oracle.cpp:97-103) at 1e-10 — the reference gates its pipeline against its naive
+// oracle at the same tolerance (ref tools/main.cpp:16, :80-86). No CPU evaluation exists here.
+// --workers / --block-size are accepted for compatibility and ignored (no CPU pool).
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/polyjac_b200.h"
+
+namespace {
+
+constexpr int64_t kConstantMemoryBytes = 65536;
+constexpr double kGateTol = 1e-10;
+constexpr uint64_t kPointSeedSalt = 0x9e3779b97f4a7c15ULL;
+
+struct Args {
+    std::string cmd;
+    std::map<std::string, std::string> kv;
+    bool help = false;
+    std::string bad;
+};
+
+Args parse(int argc, char** argv) {
+    Args a;
+    int i = 1;
+    if (i < argc && std::string(argv[i]).rfind("--", 0) != 0) a.cmd = argv[i++];
+    for (; i < argc; ++i) {
+        std::string s = argv[i];
+        if (s == "--help" || s == "-h") {
+            a.help = true;
+            continue;
+        }
+        if (s.rfind("--", 0) != 0 || i + 1 >= argc) {
+            a.bad = s;
+            break;
+        }
+        a.kv[s.substr(2)] = argv[++i];
+    }
+    return a;
+}
+
+bool get_int(const Args& a, const char* k, int64_t* v) {
+    auto it = a.kv.find(k);
+    if (it == a.kv.end()) return false;
+    char* end = nullptr;
+    *v = std::strtoll(it->second.c_str(), &end, 10);
+    return end && *end == 0;
+}
+bool get_dbl(const Args& a, const char* k, double* v) {
+    auto it = a.kv.find(k);
+    if (it == a.kv.end()) return false;
+    char* end = nullptr;
+    *v = std::strtod(it->second.c_str(), &end);
+    return end && *end == 0;
+}
+
+void usage(FILE* f) {
+    std::fprintf(f,
+                 "polyjac_b200: sparse polynomial system + Jacobian evaluator on B200 (sm_100a),\n"
+                 "complex double and complex double-double\n\n"
+                 "  generate --n N --m M --k K --d D [--seed S] --out PATH\n"
+                 "      write a random benchmark system file\n"
+                 "  bench (--system PATH | --n N --m M --k K --d D) [--seed S] [--evals E] [--points B]\n"
+                 "        [--precision dd|d] [--device G]\n"
+                 "      timed evaluation with a correctness gate; prints a RESULT key=value line\n"
+                 "  check --system PATH [--points P] [--seed S] [--tol T] [--device G]\n"
+                 "      complex double vs complex double-double on random points\n");
+}
+
+int usage_error(const std::string& msg) {
+    std::fprintf(stderr, "error: %s\n", msg.c_str());
+    usage(stderr);
+    return 2;
+}
+
+struct Sys {
+    pj_system* owned = nullptr;
+    std::vector<int32_t> pos, exps;
+    std::vector<double> coeffs;
+    pj_system_desc desc{};
+    ~Sys() { pj_system_free(owned); }
+};
+
+double cabs2(double re, double im) { return std::hypot(re, im); }
+
+// relative error in the reference's convention, the dd value rounded to double
+double rel_err(double gre, double gim, double wre, double wim) {
+    const double ag = cabs2(gre, gim), aw = cabs2(wre, wim), diff = cabs2(gre - wre, gim - wim);
+    if (ag < 1e-300 && aw < 1e-300) return diff;
+    return diff / std::max(ag, aw);
+}
+
+struct Report {
+    double max_value = 0, max_jac = 0;
+    int wv = -1, wp = -1, wi = -1;
+};
+
+// complex double vs complex dd on `B` points (host buffers): per-entry relative errors
+int compare_paths(pj_ctx* ctx, int n, const std::vector<double>& pts_d, int64_t B, Report* rep) {
+    const size_t nout = size_t(n) * n + n;
+    std::vector<double> pts_dd(size_t(B) * n * 4, 0.0), out_d(size_t(B) * nout * 2), out_dd(size_t(B) * nout * 4);
+    for (size_t i = 0; i < size_t(B) * n; ++i) {
+        pts_dd[4 * i] = pts_d[2 * i];
+        pts_dd[4 * i + 2] = pts_d[2 * i + 1];
+    }
+    int rc = pj_evaluate_host(ctx, PJ_PREC_D, pts_d.data(), B, out_d.data());
+    if (rc == PJ_OK) rc = pj_evaluate_host(ctx, PJ_PREC_DD, pts_dd.data(), B, out_dd.data());
+    if (rc != PJ_OK) return rc;
+    for (int64_t b = 0; b < B; ++b)
+        for (size_t o = 0; o < nout; ++o) {
+            const double* d = &out_d[(size_t(b) * nout + o) * 2];
+            const double* q = &out_dd[(size_t(b) * nout + o) * 4];
+            const double e = rel_err(d[0], d[1], q[0] + q[1], q[2] + q[3]);
+            if (o < size_t(n)) {
+                if (e > rep->max_value) rep->max_value = e, rep->wv = int(o);
+            } else if (e > rep->max_jac) {
+                rep->max_jac = e;
+                rep->wp = int((o - n) / n);
+                rep->wi = int((o - n) % n);
+            }
+        }
+    return PJ_OK;
+}
+
+std::string describe(const Report& r, double tol, bool pass) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "%s (tol %.3g): max value error %.3g at f[%d], max Jacobian error %.3g at J[%d][%d]",
+                  pass ? "PASS" : "FAIL", tol, r.max_value, r.wv, r.max_jac, r.wp, r.wi);
+    return buf;
+}
+
+int load_system(const Args& a, Sys& S, uint64_t seed, bool allow_generate) {
+    auto it = a.kv.find("system");
+    int64_t n, m, k, d;
+    const bool gen = get_int(a, "n", &n) && get_int(a, "m", &m) && get_int(a, "k", &k) && get_int(a, "d", &d);
+    if (it != a.kv.end()) {
+        if (a.kv.count("n") || a.kv.count("m") || a.kv.count("k") || a.kv.count("d"))
+            return usage_error("--system excludes --n --m --k --d");
+        if (pj_system_read_file(it->second.c_str(), &S.owned) != PJ_OK) {
+            std::fprintf(stderr, "error: %s\n", pj_last_error());
+            return 2;
+        }
+        pj_system_view(S.owned, &S.desc);
+        return 0;
+    }
+    if (!allow_generate) return usage_error("--system is required");
+    if (!gen) return usage_error("pass --system or all of --n --m --k --d");
+    const size_t nm = size_t(std::max<int64_t>(n, 0)) * size_t(std::max<int64_t>(m, 0));
+    S.pos.resize(nm * size_t(std::max<int64_t>(k, 1)));
+    S.exps.resize(S.pos.size());
+    S.coeffs.resize(nm * 4);
+    if (pj_random_system(int(n), int(m), int(k), int(d), seed, S.pos.data(), S.exps.data(), S.coeffs.data()) != PJ_OK) {
+        std::fprintf(stderr, "error: %s\n", pj_last_error());
+        return 2;
+    }
+    S.desc = {int32_t(n), int32_t(m), int32_t(k), int32_t(d), S.pos.data(), S.exps.data(), S.coeffs.data()};
+    return 0;
+}
+
+int cmd_generate(const Args& a) {
+    int64_t n, m, k, d, seed = 1;
+    if (!(get_int(a, "n", &n) && get_int(a, "m", &m) && get_int(a, "k", &k) && get_int(a, "d", &d)))
+        return usage_error("generate needs --n --m --k --d");
+    if (a.kv.count("seed") && !get_int(a, "seed", &seed)) return usage_error("bad --seed");
+    auto out = a.kv.find("out");
+    if (out == a.kv.end()) return usage_error("generate needs --out");
+    Args b = a;
+    b.kv.erase("out");
+    Sys S;
+    if (int rc = load_system(b, S, uint64_t(seed), true)) return rc;
+    if (pj_system_write_file(&S.desc, out->second.c_str()) != PJ_OK) {
+        std::fprintf(stderr, "error: %s\n", pj_last_error());
+        return 2;
+    }
+    std::printf("generated %s: n=%lld m=%lld k=%lld d=%lld monomials=%lld seed=%lld\n", out->second.c_str(),
+                (long long)n, (long long)m, (long long)k, (long long)d, (long long)(n * m), (long long)seed);
+    const int64_t fp = 2 * n * m * k;
+    std::printf("constant-memory footprint (positions+exponents): %lld bytes\n", (long long)fp);
+    if (fp >= kConstantMemoryBytes)
+        std::fprintf(stderr,
+                     "warning: footprint %lld bytes reaches the %lld-byte constant-memory capacity; "
+                     "positions/exponents would not fit (the B200 path keeps them in global/L2)\n",
+                     (long long)fp, (long long)kConstantMemoryBytes);
+    return 0;
+}
+
+int cmd_bench(const Args& a) {
+    int64_t seed = 1, evals = 1000, points = 65536, device = 0;
+    if (a.kv.count("seed") && !get_int(a, "seed", &seed)) return usage_error("bad --seed");
+    if (a.kv.count("evals") && (!get_int(a, "evals", &evals) || evals < 1)) return usage_error("--evals must be >= 1");
+    if (a.kv.count("points") && (!get_int(a, "points", &points) || points < 1))
+        return usage_error("--points must be >= 1");
+    if (a.kv.count("device") && !get_int(a, "device", &device)) return usage_error("bad --device");
+    std::string prec = a.kv.count("precision") ? a.kv.at("precision") : "dd";
+    if (prec != "dd" && prec != "d") return usage_error("--precision must be dd or d");
+    Sys S;
+    if (int rc = load_system(a, S, uint64_t(seed), true)) return rc;
+    pj_ctx* ctx = nullptr;
+    if (pj_ctx_create(&S.desc, int(device), &ctx) != PJ_OK) {
+        std::fprintf(stderr, "error: %s\n", pj_last_error());
+        return 2;
+    }
+    const int n = S.desc.n;
+    const int64_t B = std::min(points, evals);
+    std::vector<double> pts(size_t(B) * n * 2);
+    pj_random_points(n, B, uint64_t(seed) ^ kPointSeedSalt, pts.data());
+    // correctness gate before any timing is reported
+    Report gate;
+    if (int rc = compare_paths(ctx, n, pts, std::min<int64_t>(B, 64), &gate)) {
+        std::fprintf(stderr, "error: %s\n", pj_last_error());
+        pj_ctx_destroy(ctx);
+        return 2;
+    }
+    const bool ok = gate.max_value <= kGateTol && gate.max_jac <= kGateTol;
+    if (!ok) {
+        std::fprintf(stderr, "correctness gate failed: %s\n", describe(gate, kGateTol, false).c_str());
+        pj_ctx_destroy(ctx);
+        return 1;
+    }
+    // device-resident timing of `evals` evaluations in batches of B points, each precision
+    const size_t nout = size_t(n) * n + n;
+    auto time_prec = [&](int flags, int W, double* ms) -> int {
+        double *dp = nullptr, *dout = nullptr;
+        std::vector<double> host(size_t(B) * n * W, 0.0);
+        for (size_t i = 0; i < size_t(B) * n; ++i) {
+            host[W * i] = pts[2 * i];
+            host[W * i + (W == 4 ? 2 : 1)] = pts[2 * i + 1];
+        }
+        if (cudaSetDevice(int(device)) || cudaMalloc(&dp, host.size() * 8) || cudaMalloc(&dout, size_t(B) * nout * W * 8) ||
+            cudaMemcpy(dp, host.data(), host.size() * 8, cudaMemcpyHostToDevice))
+            return PJ_ECUDA;
+        int rc = pj_evaluate(ctx, flags, dp, B, dout, nullptr);  // warm-up
+        cudaEvent_t e0, e1;
+        cudaEventCreate(&e0);
+        cudaEventCreate(&e1);
+        cudaEventRecord(e0);
+        for (int64_t done = 0; done < evals && rc == PJ_OK; done += B)
+            rc = pj_evaluate(ctx, flags, dp, std::min(B, evals - done), dout, nullptr);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float f = 0;
+        cudaEventElapsedTime(&f, e0, e1);
+        *ms = f;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        cudaFree(dp);
+        cudaFree(dout);
+        return rc;
+    };
+    double ms_d = 0, ms_dd = 0;
+    int rc = time_prec(PJ_PREC_D, 2, &ms_d);
+    if (rc == PJ_OK && prec == "dd") rc = time_prec(PJ_PREC_DD, 4, &ms_dd);
+    if (rc != PJ_OK) {
+        std::fprintf(stderr, "error: %s\n", pj_last_error());
+        pj_ctx_destroy(ctx);
+        return 2;
+    }
+    const double ms = prec == "dd" ? ms_dd : ms_d;
+    uint64_t cnt[5];
+    pj_mult_counts(ctx, evals, cnt);
+    int32_t threads = 0, tp = 0, blocks = 0, var = 0;
+    int64_t smem = 0;
+    pj_get_launch(ctx, prec == "dd" ? PJ_PREC_DD : PJ_PREC_D, &threads, &tp, &blocks, &smem, &var);
+    const long long mults = (long long)(cnt[0] + cnt[1] + cnt[2] + cnt[4]);
+    std::printf("system: n=%d m=%d k=%d d=%d (%lld monomials), footprint %lld bytes\n", S.desc.n, S.desc.m, S.desc.k,
+                S.desc.d, (long long)S.desc.n * S.desc.m, 2LL * S.desc.n * S.desc.m * S.desc.k);
+    std::printf("device %lld: %d-thread CTAs x %d, %lld evaluations in batches of %lld points\n", (long long)device,
+                threads, blocks, (long long)evals, (long long)B);
+    std::printf("gate: %s\n", describe(gate, kGateTol, true).c_str());
+    std::printf("complex double (reference order): %.3f ms; requested %s: %.3f ms (%.3e evals/s)\n", ms_d, prec.c_str(),
+                ms, evals / (ms * 1e-3));
+    std::printf("RESULT n=%d m=%d k=%d d=%d monomials=%lld B=%d workers=1 evals=%lld baseline_ms=%.3f pipeline_ms=%.3f "
+                "speedup=%.3f mults=%lld footprint_bytes=%lld precision=%s points=%lld evals_per_s=%.6g gate_max_rel=%.3g\n",
+                S.desc.n, S.desc.m, S.desc.k, S.desc.d, (long long)S.desc.n * S.desc.m, threads, (long long)evals, ms_d,
+                ms, ms > 0 ? ms_d / ms : 0.0, mults, 2LL * S.desc.n * S.desc.m * S.desc.k, prec.c_str(), (long long)B,
+                evals / (ms * 1e-3), std::max(gate.max_value, gate.max_jac));
+    pj_ctx_destroy(ctx);
+    return 0;
+}
+
+int cmd_check(const Args& a) {
+    int64_t points = 100, seed = 1, device = 0;
+    double tol = 1e-10;
+    if (a.kv.count("points") && (!get_int(a, "points", &points) || points < 1))
+        return usage_error("--points must be >= 1");
+    if (a.kv.count("seed") && !get_int(a, "seed", &seed)) return usage_error("bad --seed");
+    if (a.kv.count("tol") && (!get_dbl(a, "tol", &tol) || !(tol > 0))) return usage_error("--tol must be > 0");
+    if (a.kv.count("device") && !get_int(a, "device", &device)) return usage_error("bad --device");
+    Sys S;
+    if (int rc = load_system(a, S, uint64_t(seed), false)) return rc;
+    pj_ctx* ctx = nullptr;
+    if (pj_ctx_create(&S.desc, int(device), &ctx) != PJ_OK) {
+        std::fprintf(stderr, "error: %s\n", pj_last_error());
+        return 2;
+    }
+    std::vector<double> pts(size_t(points) * S.desc.n * 2);
+    pj_random_points(S.desc.n, points, uint64_t(seed) ^ kPointSeedSalt, pts.data());
+    Report r;
+    if (compare_paths(ctx, S.desc.n, pts, points, &r) != PJ_OK) {
+        std::fprintf(stderr, "error: %s\n", pj_last_error());
+        pj_ctx_destroy(ctx);
+        return 2;
+    }
+    pj_ctx_destroy(ctx);
+    const bool pass = r.max_value <= tol && r.max_jac <= tol;
+    std::printf("checked %lld random points: %s\n", (long long)points, describe(r, tol, pass).c_str());
+    return pass ? 0 : 1;
+}
+
+}  // namespace
+
+int main(int argc, char** argv) {
+    Args a = parse(argc, argv);
+    if (a.help || (a.cmd.empty() && argc > 1 && a.bad.empty())) {
+        usage(stdout);
+        return 0;
+    }
+    if (!a.bad.empty()) return usage_error("unexpected argument " + a.bad);
+    if (a.cmd == "generate") return cmd_generate(a);
+    if (a.cmd == "bench") return cmd_bench(a);
+    if (a.cmd == "check") return cmd_check(a);
+    return usage_error(a.cmd.empty() ? "a subcommand is required" : "unknown subcommand " + a.cmd);
+}

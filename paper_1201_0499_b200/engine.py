@@ -164,6 +164,49 @@ def to_dd(points) -> np.ndarray:
     return out
 
 
+# --------------------------------------------------------------------------- system files
+def _from_handle(h) -> PolynomialSystem:
+    desc = SystemDesc()
+    check(lib().pj_system_view(h, ctypes.byref(desc)))
+    n, m, k = desc.n, desc.m, desc.k
+    nm = n * m
+    pos = np.ctypeslib.as_array(ctypes.cast(desc.positions, ctypes.POINTER(ctypes.c_int32)), (nm * k,)).copy()
+    exps = np.ctypeslib.as_array(ctypes.cast(desc.exponents, ctypes.POINTER(ctypes.c_int32)), (nm * k,)).copy()
+    co = np.ctypeslib.as_array(ctypes.cast(desc.coeffs, ctypes.POINTER(ctypes.c_double)), (nm * 4,)).copy()
+    lib().pj_system_free(h)
+    return PolynomialSystem(n, m, k, desc.d, pos.reshape(nm, k), exps.reshape(nm, k), co.reshape(nm, 4))
+
+
+def read_system(path: str) -> PolynomialSystem:
+    """ref src/io.cpp:115-119; FormatError ("path:line: what") on malformed input."""
+    h = ctypes.c_void_p()
+    check(lib().pj_system_read_file(path.encode(), ctypes.byref(h)))
+    return _from_handle(h)
+
+
+def read_system_text(text: str, name: str = "<stream>") -> PolynomialSystem:
+    """ref src/io.cpp:38-98 on an in-memory text."""
+    h = ctypes.c_void_p()
+    check(lib().pj_system_read_text(text.encode(), name.encode(), ctypes.byref(h)))
+    return _from_handle(h)
+
+
+def write_system_text(sys: PolynomialSystem) -> str:
+    """ref src/io.cpp:100-108: doubles with 17 significant digits, 1-based positions."""
+    desc, keep = sys._desc()
+    ln = lib().pj_system_write_text(ctypes.byref(desc), None, 0)
+    if ln < 0:
+        check(_lib.PJ_EINVAL)
+    buf = ctypes.create_string_buffer(ln + 1)
+    lib().pj_system_write_text(ctypes.byref(desc), buf, ln + 1)
+    return buf.value.decode()
+
+
+def write_system(sys: PolynomialSystem, path: str) -> None:
+    desc, keep = sys._desc()
+    check(lib().pj_system_write_file(ctypes.byref(desc), path.encode()))
+
+
 def mons_slot(s: int, kind: str, var: int, n: int, m: int) -> int:
     """ref src/packing.cpp:8-17; IndexError where the reference throws std::out_of_range."""
     out = ctypes.c_int64(0)
