@@ -128,6 +128,33 @@ int pj_system_write_file(const pj_system_desc* sys, const char* path);
 /* Writes the text into buf (capacity cap, NUL-terminated, may be NULL); returns its full length. */
 int64_t pj_system_write_text(const pj_system_desc* sys, char* buf, int64_t cap);
 
+/* Newton corrector on device (the consumer of the evaluator's output — the
+ * reference leaves Newton / path tracking out of scope, ref SPEC.md:12, so the operation order is
+ * defined in csrc/newton.cu and restated by the oracle). For every point b:
+ *     J_b dx = y_b - f_b   (Gaussian elimination, partial pivoting on |Re hi| + |Im hi|),
+ *     x_new_b = x_b + dx,
+ * in the precision of `flags` (PJ_PREC_D or PJ_PREC_DD; the order bits are ignored).
+ *   evals       [batch][n + n*n][W]  pj_evaluate's output at `points` (read only)
+ *   points      [batch][n][W]
+ *   target      [batch][n][W] or NULL (y = 0: the roots of f)
+ *   points_out  [batch][n][W]; may alias points (in-place update)
+ *   norms       [batch][2] or NULL: max over i of max(|Re hi|, |Im hi|) of (y - f)_i, of dx_i
+ *   status      [batch] or NULL: 0 ok, 1 singular (a zero pivot column; x_new = x, norms[1] = inf),
+ *               2 non-finite result
+ * Asynchronous on `stream`; no allocation for n <= 64 (larger n allocates per-CTA matrix slabs
+ * on first use). */
+int pj_newton_solve(pj_ctx* ctx, int flags, const double* d_evals, const double* d_points, const double* d_target,
+                    int64_t batch, double* d_points_out, double* d_norms, int32_t* d_status, void* stream);
+/* One Newton step: pj_evaluate(points -> work) then pj_newton_solve(work). work: [batch][n + n*n][W],
+ * caller-owned; on return it holds f and J at the input points. */
+int pj_newton_step(pj_ctx* ctx, int flags, const double* d_points, const double* d_target, int64_t batch,
+                   double* d_work, double* d_points_out, double* d_norms, int32_t* d_status, void* stream);
+/* Host-buffer convenience: `iters` Newton steps per point on device (chunks whose evaluator
+ * output stays L2-resident), synchronous; norms/status describe the last step. Returns
+ * PJ_ENONFINITE when an input coordinate is non-finite (like pj_evaluate_host). */
+int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double* h_target, int64_t batch, int iters,
+                   double* h_points_out, double* h_norms, int32_t* h_status);
+
 /* Advanced: override the launch shape for `flags`' precision (threads per CTA, multiple of 32,
  * <= 256; points per CTA tile). 0 restores the automatic choice. */
 int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points);

@@ -295,6 +295,146 @@ void evaluate_range(const System& S, const double* pts, long b0, long b1, double
     }
 }
 
+
+// ------------------------------------------------------------------ Newton corrector (f1)
+// Restates the operation order defined in paper_1201_0499_b200/csrc/newton.cu (the reference
+// has no Newton step): rhs = y + (-f); Gaussian elimination with partial pivoting
+// on |Re hi| + |Im hi| (first maximum, strictly positive); pivot inverse conj(a)/|a|^2;
+// multipliers l = A[i][kk] * inv (normalised product); trailing update
+// A[i][j] + (-(l * A[kk][j])) with the dd product left unnormalised; back substitution
+// dx_i = rhs_i * inv_i, rhs_r + (-(A[r][i] * dx_i)) for r < i (descending i); x + dx.
+// The dd pieces are restated from their published algorithms (Dekker product with FMA,
+// Newton-corrected reciprocal), independently of the device copy.
+static inline CDD cdd_mul_u(CDD a, CDD b) {  // product without the closing Fast2Sum
+    CDD r;
+    {
+        double p1 = a.rh * b.rh, e1 = std::fma(a.rh, b.rh, -p1);
+        double p2 = a.ih * b.ih, e2 = std::fma(a.ih, b.ih, -p2);
+        DD st = two_sum(p1, -p2);
+        double la = std::fma(a.rh, b.rl, e1);
+        la = std::fma(a.rl, b.rh, la);
+        double lb = std::fma(a.ih, b.il, e2);
+        lb = std::fma(a.il, b.ih, lb);
+        r.rh = st.hi;
+        r.rl = (la - lb) + st.lo;
+    }
+    {
+        double p3 = a.rh * b.ih, e3 = std::fma(a.rh, b.ih, -p3);
+        double p4 = a.ih * b.rh, e4 = std::fma(a.ih, b.rh, -p4);
+        DD st = two_sum(p3, p4);
+        double lc = std::fma(a.rh, b.il, e3);
+        lc = std::fma(a.rl, b.ih, lc);
+        double ld = std::fma(a.ih, b.rl, e4);
+        ld = std::fma(a.il, b.rh, ld);
+        r.ih = st.hi;
+        r.il = (lc + ld) + st.lo;
+    }
+    return r;
+}
+static inline DD dd_mul(DD a, DD b) {
+    double p = a.hi * b.hi;
+    double e = std::fma(a.hi, b.hi, -p);
+    e = std::fma(a.hi, b.lo, e);
+    e = std::fma(a.lo, b.hi, e);
+    return fast_two_sum(p, e);
+}
+static inline DD dd_rcp(DD a) {
+    double q = 1.0 / a.hi;
+    double t = std::fma(-a.hi, q, 1.0);
+    t = std::fma(-a.lo, q, t);
+    return fast_two_sum(q, t * q);
+}
+struct NT_D {
+    using T = CD;
+    static constexpr int W = 2;
+    static CD neg(CD a) { return {-a.re, -a.im}; }
+    static double mag1(CD a) { return std::fabs(a.re) + std::fabs(a.im); }
+    static double magmax(CD a) { return std::fmax(std::fabs(a.re), std::fabs(a.im)); }
+    static bool finite(CD a) { return std::isfinite(a.re) && std::isfinite(a.im); }
+    static CD umul(CD a, CD b) { return cd_mul(a, b); }
+    static CD inv(CD a) {
+        double den = a.re * a.re + a.im * a.im;
+        double r = 1.0 / den;
+        return {a.re * r, -a.im * r};
+    }
+};
+struct NT_DD {
+    using T = CDD;
+    static constexpr int W = 4;
+    static CDD neg(CDD a) { return {-a.rh, -a.rl, -a.ih, -a.il}; }
+    static double mag1(CDD a) { return std::fabs(a.rh) + std::fabs(a.ih); }
+    static double magmax(CDD a) { return std::fmax(std::fabs(a.rh), std::fabs(a.ih)); }
+    static bool finite(CDD a) {
+        return std::isfinite(a.rh) && std::isfinite(a.rl) && std::isfinite(a.ih) && std::isfinite(a.il);
+    }
+    static CDD umul(CDD a, CDD b) { return cdd_mul_u(a, b); }
+    static CDD inv(CDD a) {
+        DD re{a.rh, a.rl}, im{a.ih, a.il};
+        DD den = dd_add(dd_mul(re, re), dd_mul(im, im));
+        DD r = dd_rcp(den);
+        DD o = dd_mul(re, r), p = dd_mul({-a.ih, -a.il}, r);
+        return {o.hi, o.lo, p.hi, p.lo};
+    }
+};
+
+template <class NT>
+void newton_one(int n, const double* ev, const double* x, const double* y, double* xo, double* norms, int* status) {
+    using T = typename NT::T;
+    using O = Ops<T>;
+    constexpr int W = NT::W;
+    const int ld = n + 1;
+    std::vector<T> A(size_t(n) * ld), inv(n);
+    double rn = 0.0;
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < n; ++j) A[size_t(i) * ld + j] = O::load(ev + size_t(n + i * n + j) * W);
+        T r = NT::neg(O::load(ev + size_t(i) * W));
+        if (y) r = O::add(O::load(y + size_t(i) * W), r);
+        A[size_t(i) * ld + n] = r;
+        rn = std::fmax(rn, NT::magmax(r));
+    }
+    if (norms) norms[0] = rn;
+    auto at = [&](int i, int j) -> T& { return A[size_t(i) * ld + j]; };
+    for (int kk = 0; kk < n; ++kk) {
+        double best = 0.0;
+        int bi = -1;
+        for (int i = kk; i < n; ++i) {
+            const double mg = NT::mag1(at(i, kk));
+            if (mg > best) {
+                best = mg;
+                bi = i;
+            }
+        }
+        if (bi < 0) {
+            for (int i = 0; i < n; ++i) O::store(xo + size_t(i) * W, O::load(x + size_t(i) * W));
+            if (norms) norms[1] = INFINITY;
+            if (status) *status = 1;
+            return;
+        }
+        if (bi != kk)
+            for (int j = kk; j <= n; ++j) std::swap(at(kk, j), at(bi, j));
+        inv[kk] = NT::inv(at(kk, kk));
+        for (int i = kk + 1; i < n; ++i) at(i, kk) = O::mul(at(i, kk), inv[kk]);
+        for (int i = kk + 1; i < n; ++i)
+            for (int j = kk + 1; j <= n; ++j) at(i, j) = O::add(at(i, j), NT::neg(NT::umul(at(i, kk), at(kk, j))));
+    }
+    std::vector<T> rhs(n);
+    for (int i = 0; i < n; ++i) rhs[i] = at(i, n);
+    for (int i = n - 1; i >= 0; --i) {
+        const T dx = O::mul(rhs[i], inv[i]);
+        rhs[i] = dx;
+        for (int r = 0; r < i; ++r) rhs[r] = O::add(rhs[r], NT::neg(NT::umul(at(r, i), dx)));
+    }
+    double dn = 0.0;
+    bool fin = true;
+    for (int i = 0; i < n; ++i) {
+        const T xn = O::add(O::load(x + size_t(i) * W), rhs[i]);
+        O::store(xo + size_t(i) * W, xn);
+        dn = std::fmax(dn, NT::magmax(rhs[i]));
+        fin = fin && NT::finite(xn);
+    }
+    if (norms) norms[1] = dn;
+    if (status) *status = fin ? 0 : 2;
+}
 }  // namespace oracle
 
 extern "C" {
@@ -396,6 +536,40 @@ long long oracle_zero_mask(int n, int m, int k, const int* pos, long long* mask)
     for (long long i = 0; i < stride * m; ++i)
         if (!claimed[size_t(i)]) mask[len++] = i;
     return len;
+}
+
+// Newton corrector restatement (see newton_one): evals [B][n+n*n][W], points/target/out
+// [B][n][W] (target nullable), norms [B][2] and status [B] nullable.
+int oracle_newton_solve(int prec, int n, const double* evals, const double* points, const double* target, long B,
+                        double* out, double* norms, int* status, int threads) {
+    if (prec != 1 && prec != 2) return 1;
+    const int W = prec == 1 ? 2 : 4;
+    const size_t nout = size_t(n) * n + n;
+    if (threads < 1) threads = 1;
+    if (threads > B) threads = B > 0 ? int(B) : 1;
+    auto work = [&](int t) {
+        long b0 = B * t / threads, b1 = B * (t + 1) / threads;
+        for (long b = b0; b < b1; ++b) {
+            const double* ev = evals + size_t(b) * nout * W;
+            const double* x = points + size_t(b) * n * W;
+            const double* y = target ? target + size_t(b) * n * W : nullptr;
+            double* xo = out + size_t(b) * n * W;
+            double* nr = norms ? norms + 2 * b : nullptr;
+            int* st = status ? status + b : nullptr;
+            if (prec == 1)
+                oracle::newton_one<oracle::NT_D>(n, ev, x, y, xo, nr, st);
+            else
+                oracle::newton_one<oracle::NT_DD>(n, ev, x, y, xo, nr, st);
+        }
+    };
+    if (threads == 1) {
+        work(0);
+    } else {
+        std::vector<std::thread> th;
+        for (int t = 0; t < threads; ++t) th.emplace_back(work, t);
+        for (auto& t : th) t.join();
+    }
+    return 0;
 }
 
 }  // extern "C"

@@ -65,6 +65,9 @@ def lib():
         L.oracle_mons_slot.restype = ctypes.c_longlong
         L.oracle_zero_mask.argtypes = [ctypes.c_int] * 3 + [_i32p, _i64p]
         L.oracle_zero_mask.restype = ctypes.c_longlong
+        L.oracle_newton_solve.argtypes = [ctypes.c_int, ctypes.c_int, _f64p, _f64p, ctypes.c_void_p, ctypes.c_long,
+                                          _f64p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
+        L.oracle_newton_solve.restype = ctypes.c_int
         _oracle = L
     return _oracle
 
@@ -135,6 +138,28 @@ def evaluate(prec, sysd, points, threads=1, magsum=False, counts=False):
     if counts:
         res.append(dict(zip(["powers", "factors", "stage2", "speelpenning", "stage3"], list(cnt))))
     return res[0] if len(res) == 1 else tuple(res)
+
+
+def newton_solve(prec, n, evals, points, target=None, threads=1):
+    """CPU restatement of the Newton corrector (paper_1201_0499_b200/csrc/newton.cu): per point
+    solve J dx = y - f from the evaluator's output and return (x + dx, norms [B, 2], status [B])."""
+    W = 2 if prec == "d" else 4
+    ev = np.ascontiguousarray(evals, np.float64)
+    pts = np.ascontiguousarray(points, np.float64)
+    B = pts.shape[0]
+    assert pts.shape == (B, n, W) and ev.shape == (B, n + n * n, W), (pts.shape, ev.shape)
+    tg = None
+    if target is not None:
+        tg = np.ascontiguousarray(target, np.float64)
+        assert tg.shape == pts.shape
+    out = np.empty_like(pts)
+    norms = np.empty((B, 2), np.float64)
+    status = np.empty(B, np.int32)
+    rc = lib().oracle_newton_solve(1 if prec == "d" else 2, n, ev, pts, tg.ctypes.data if tg is not None else None,
+                                   B, out, norms.ctypes.data, status.ctypes.data, threads)
+    if rc:
+        raise RuntimeError("oracle_newton_solve failed")
+    return out, norms, status
 
 
 def speelpenning(prec, vals):

@@ -22,7 +22,7 @@ EXPORTS = [
     "pj_zero_mask", "pj_mult_counts", "pj_random_system", "pj_random_points", "pj_set_launch",
     "pj_get_launch", "pj_fp64_peak_probe", "pj_random_points_range", "pj_set_kernel_variant",
     "pj_system_read_file", "pj_system_read_text", "pj_system_view", "pj_system_free", "pj_system_write_file",
-    "pj_system_write_text",
+    "pj_system_write_text", "pj_newton_solve", "pj_newton_step", "pj_newton_host",
 ]
 
 
@@ -81,6 +81,9 @@ def lib():
     L.pj_system_write_file.argtypes = [ctypes.POINTER(SystemDesc), ctypes.c_char_p]
     L.pj_system_write_text.argtypes = [ctypes.POINTER(SystemDesc), ctypes.c_char_p, i64]
     L.pj_system_write_text.restype = i64
+    L.pj_newton_solve.argtypes = [vp, ctypes.c_int, vp, vp, vp, i64, vp, vp, vp, vp]
+    L.pj_newton_step.argtypes = [vp, ctypes.c_int, vp, vp, i64, vp, vp, vp, vp, vp]
+    L.pj_newton_host.argtypes = [vp, ctypes.c_int, vp, vp, i64, ctypes.c_int, vp, vp, vp]
     L.pj_fp64_peak_probe.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     for name in EXPORTS:
         getattr(L, name)  # fail loudly on a stale library

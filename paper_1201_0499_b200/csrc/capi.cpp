@@ -144,6 +144,18 @@ struct pj_ctx {
     size_t in_cap = 0, out_cap = 0;
     cudaStream_t hstream[kHostStreams] = {};
     cudaEvent_t hdone[kHostStreams] = {};
+    // Newton corrector (f1): launch shape per precision, global matrix slabs when the
+    // augmented matrix exceeds shared memory, host-API staging buffers
+    struct NewtonPlan {
+        int blocks = 0, threads = 0;
+        size_t smem = 0;
+        bool gscr = false;
+    } newton[2];
+    double* d_nscratch = nullptr;
+    size_t nscratch_bytes = 0;
+    double *d_nx = nullptr, *d_nwork = nullptr, *d_ntgt = nullptr, *d_nnorm = nullptr;
+    int* d_nstat = nullptr;
+    size_t nx_cap = 0, nwork_cap = 0;
 
     pjb::DevSystem dev(int pi) const {
         pjb::DevSystem S;
@@ -189,6 +201,12 @@ void free_ctx(pj_ctx* c) {
     cudaFree(c->d_coef[1]);
     cudaFree(c->d_coefT);
     cudaFree(c->d_scratch);
+    cudaFree(c->d_nscratch);
+    cudaFree(c->d_nx);
+    cudaFree(c->d_nwork);
+    cudaFree(c->d_ntgt);
+    cudaFree(c->d_nnorm);
+    cudaFree(c->d_nstat);
     for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
         cudaFree(c->d_in[i]);
         cudaFree(c->d_out[i]);
@@ -828,6 +846,172 @@ int pj_get_launch(pj_ctx* ctx, int flags, int32_t* threads, int32_t* tile_points
     if (blocks) *blocks = L.blocks;
     if (smem_bytes) *smem_bytes = int64_t(L.smem_bytes);
     if (variant) *variant = L.variant;
+    g_err.clear();
+    return PJ_OK;
+}
+
+
+// ------------------------------------------------------------------ Newton corrector (f1)
+namespace {
+int newton_plan(pj_ctx* c, int pi, pj_ctx::NewtonPlan** out) {
+    pj_ctx::NewtonPlan& P = c->newton[pi];
+    const int prec = pi + 1;
+    const size_t mb = pjb::newton_matrix_bytes(prec, c->n);
+    if (!P.blocks) {
+        P.threads = 256;
+        if (mb <= c->smem_optin) {
+            const int nb = pjb::newton_blocks_per_sm(prec, c->n, P.threads, mb);
+            if (nb > 0) {
+                P.smem = mb;
+                P.blocks = nb * c->sms;
+                P.gscr = false;
+            }
+        }
+        if (!P.blocks) {  // augmented matrix beyond shared memory: per-CTA slabs in HBM (L2-resident)
+            const int nb = std::max(1, std::min(pjb::newton_blocks_per_sm(prec, c->n, P.threads, 0), 4));
+            P.smem = 0;
+            P.blocks = nb * c->sms;
+            P.gscr = true;
+        }
+    }
+    if (P.gscr) {
+        const size_t stride = (mb / sizeof(double) + 31) / 32 * 32;
+        const size_t need = stride * sizeof(double) * size_t(P.blocks);
+        if (need > c->nscratch_bytes) {
+            cudaFree(c->d_nscratch);
+            c->d_nscratch = nullptr;
+            c->nscratch_bytes = 0;
+            PJ_CUDA(cudaMalloc(&c->d_nscratch, need));
+            c->nscratch_bytes = need;
+        }
+    }
+    *out = &P;
+    return PJ_OK;
+}
+}  // namespace
+
+int pj_newton_solve(pj_ctx* ctx, int flags, const double* d_evals, const double* d_points, const double* d_target,
+                    int64_t batch, double* d_points_out, double* d_norms, int32_t* d_status, void* stream) {
+    if (!ctx) return fail(PJ_EINVAL, "null context");
+    const int pi = prec_index(flags);
+    if (pi < 0) return fail(PJ_EINVAL, "newton: unknown precision flag");
+    if (batch < 0) return fail(PJ_EINVAL, "newton: negative batch");
+    if (batch == 0) {
+        g_err.clear();
+        return PJ_OK;
+    }
+    if (!d_evals || !d_points || !d_points_out) return fail(PJ_EINVAL, "newton: null buffer");
+    if (ctx->host_only) return fail(PJ_EINVAL, "newton: host-only context (created with device < 0)");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != ctx->device) PJ_CUDA(cudaSetDevice(ctx->device));
+    pj_ctx::NewtonPlan* P = nullptr;
+    int rc = newton_plan(ctx, pi, &P);
+    if (rc) {
+        if (prev != ctx->device) cudaSetDevice(prev);
+        return rc;
+    }
+    pjb::NewtonArgs a;
+    a.n = ctx->n;
+    a.B = batch;
+    a.evals = d_evals;
+    a.points = d_points;
+    a.target = d_target;
+    a.points_out = d_points_out;
+    a.norms = d_norms;
+    a.status = d_status;
+    a.gscratch = P->gscr ? ctx->d_nscratch : nullptr;
+    a.gstride = (pjb::newton_matrix_bytes(pi + 1, ctx->n) / sizeof(double) + 31) / 32 * 32;
+    cudaError_t e = pjb::launch_newton(pi + 1, a, P->blocks, P->threads, P->smem, (cudaStream_t)stream);
+    if (prev != ctx->device) cudaSetDevice(prev);
+    if (e) return cuda_fail(e, "newton: kernel launch");
+    g_err.clear();
+    return PJ_OK;
+}
+
+int pj_newton_step(pj_ctx* ctx, int flags, const double* d_points, const double* d_target, int64_t batch,
+                   double* d_work, double* d_points_out, double* d_norms, int32_t* d_status, void* stream) {
+    if (batch > 0 && !d_work) return fail(PJ_EINVAL, "newton: null buffer");
+    int rc = pj_evaluate(ctx, flags, d_points, batch, d_work, stream);
+    if (rc) return rc;
+    return pj_newton_solve(ctx, flags, d_work, d_points, d_target, batch, d_points_out, d_norms, d_status, stream);
+}
+
+int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double* h_target, int64_t batch, int iters,
+                   double* h_points_out, double* h_norms, int32_t* h_status) {
+    if (!ctx) return fail(PJ_EINVAL, "null context");
+    const int pi = prec_index(flags);
+    if (pi < 0) return fail(PJ_EINVAL, "newton: unknown precision flag");
+    if (batch < 0) return fail(PJ_EINVAL, "newton: negative batch");
+    if (iters < 1) return fail(PJ_EINVAL, "newton: iterations must be >= 1");
+    if (batch == 0) {
+        g_err.clear();
+        return PJ_OK;
+    }
+    if (!h_points || !h_points_out) return fail(PJ_EINVAL, "newton: null buffer");
+    if (ctx->host_only) return fail(PJ_EINVAL, "newton: host-only context (created with device < 0)");
+    const int W = pi == 0 ? 2 : 4;
+    const size_t x_pt = size_t(ctx->n) * W * 8;
+    const size_t out_pt = (size_t(ctx->n) * ctx->n + ctx->n) * W * 8;
+    // chunk: the evaluator's output for one chunk stays L2-resident (<= 96 MiB) between the
+    // evaluation and the solve; whole evaluation waves when the chunk spans more than one
+    const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
+    const int64_t wave = std::max<int64_t>(int64_t(L.blocks) * L.tp, 1);
+    int64_t chunk = std::max<int64_t>(int64_t((96ull << 20) / out_pt), 1);
+    if (chunk > wave) chunk = chunk / wave * wave;
+    chunk = std::min<int64_t>(chunk, batch);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    PJ_CUDA(cudaSetDevice(ctx->device));
+    if (size_t(chunk) * x_pt > ctx->nx_cap || size_t(chunk) * out_pt > ctx->nwork_cap) {
+        cudaFree(ctx->d_nx);
+        cudaFree(ctx->d_nwork);
+        cudaFree(ctx->d_ntgt);
+        cudaFree(ctx->d_nnorm);
+        cudaFree(ctx->d_nstat);
+        ctx->d_nx = ctx->d_nwork = ctx->d_ntgt = ctx->d_nnorm = nullptr;
+        ctx->d_nstat = nullptr;
+        ctx->nx_cap = ctx->nwork_cap = 0;
+        PJ_CUDA(cudaMalloc(&ctx->d_nx, size_t(chunk) * x_pt));
+        PJ_CUDA(cudaMalloc(&ctx->d_ntgt, size_t(chunk) * x_pt));
+        PJ_CUDA(cudaMalloc(&ctx->d_nwork, size_t(chunk) * out_pt));
+        PJ_CUDA(cudaMalloc(&ctx->d_nnorm, size_t(chunk) * 2 * sizeof(double)));
+        PJ_CUDA(cudaMalloc(&ctx->d_nstat, size_t(chunk) * sizeof(int32_t)));
+        ctx->nx_cap = size_t(chunk) * x_pt;
+        ctx->nwork_cap = size_t(chunk) * out_pt;
+    }
+    cudaStream_t st = ctx->hstream[0];
+    int rc = PJ_OK;
+    for (int64_t b0 = 0; b0 < batch && rc == PJ_OK; b0 += chunk) {
+        const int64_t nb = std::min<int64_t>(chunk, batch - b0);
+        PJ_CUDA(cudaMemcpyAsync(ctx->d_nx, reinterpret_cast<const char*>(h_points) + size_t(b0) * x_pt,
+                                size_t(nb) * x_pt, cudaMemcpyHostToDevice, st));
+        if (h_target)
+            PJ_CUDA(cudaMemcpyAsync(ctx->d_ntgt, reinterpret_cast<const char*>(h_target) + size_t(b0) * x_pt,
+                                    size_t(nb) * x_pt, cudaMemcpyHostToDevice, st));
+        for (int it = 0; it < iters && rc == PJ_OK; ++it)
+            rc = pj_newton_step(ctx, flags, ctx->d_nx, h_target ? ctx->d_ntgt : nullptr, nb, ctx->d_nwork, ctx->d_nx,
+                                ctx->d_nnorm, ctx->d_nstat, st);
+        if (rc) break;
+        PJ_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(h_points_out) + size_t(b0) * x_pt, ctx->d_nx,
+                                size_t(nb) * x_pt, cudaMemcpyDeviceToHost, st));
+        if (h_norms)
+            PJ_CUDA(cudaMemcpyAsync(h_norms + 2 * b0, ctx->d_nnorm, size_t(nb) * 2 * sizeof(double),
+                                    cudaMemcpyDeviceToHost, st));
+        if (h_status)
+            PJ_CUDA(cudaMemcpyAsync(h_status + b0, ctx->d_nstat, size_t(nb) * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                    st));
+        PJ_CUDA(cudaStreamSynchronize(st));  // the staging buffers are reused by the next chunk
+    }
+    if (rc) {
+        cudaSetDevice(prev);
+        return rc;
+    }
+    int seen = 0;
+    rc = pj_nonfinite_seen(ctx, st, &seen);
+    cudaSetDevice(prev);
+    if (rc) return rc;
+    if (seen) return fail(PJ_ENONFINITE, "evaluate: non-finite coordinate");
     g_err.clear();
     return PJ_OK;
 }

@@ -64,4 +64,22 @@ cudaError_t launch_fast(int k, const LaunchCfg& L, const DevSystem& S, const dou
                         cudaStream_t st);
 int fast_blocks_per_sm(int k, int n, int d, int threads, size_t smem);
 
+// Newton corrector (newton.cu): per point, solve J dx = y - f from the
+// evaluator's output and write x + dx
+struct NewtonArgs {
+    int n;
+    long long B;
+    const double* evals;   // [B][n + n*n][W] (pj_evaluate output)
+    const double* points;  // [B][n][W]
+    const double* target;  // [B][n][W] or null (y = 0)
+    double* points_out;    // [B][n][W] (may alias points)
+    double* norms;         // [B][2] or null: max-norm of y - f, of dx (high words)
+    int* status;           // [B] or null: 0 ok, 1 singular, 2 non-finite result
+    double* gscratch;      // non-null: per-CTA matrix slabs in global memory (gstride doubles each)
+    size_t gstride;
+};
+size_t newton_matrix_bytes(int prec, int n);
+int newton_blocks_per_sm(int prec, int n, int threads, size_t smem);
+cudaError_t launch_newton(int prec, const NewtonArgs& args, int blocks, int threads, size_t smem, cudaStream_t st);
+
 }  // namespace pjb

@@ -421,6 +421,67 @@ class EvaluationContext:
         check(lib().pj_nonfinite_seen(self._h, ctypes.c_void_p(stream or 0), ctypes.byref(seen)))
         return bool(seen.value)
 
+    # ---- Newton corrector (csrc/newton.cu)
+    def newton_host(self, points: np.ndarray, precision: str = "dd", iters: int = 1, target: np.ndarray | None = None,
+                    order: str | None = None):
+        """`iters` Newton steps x <- x + J(x)^-1 (y - f(x)) per point, on the GPU.
+        points (and target y, optional; absent = the roots of f): [B, n, W] float64.
+        Returns (points_out [B, n, W], norms [B, 2] = max-norms of y - f and of the last step,
+        status [B] int32: 0 ok, 1 singular Jacobian, 2 non-finite result)."""
+        W = 2 if precision == "d" else 4
+        pts = np.ascontiguousarray(points, np.float64)
+        if pts.ndim != 3 or pts.shape[1:] != (self.n, W):
+            raise ValueError("newton: point dimension mismatch")
+        tg = None
+        if target is not None:
+            tg = np.ascontiguousarray(target, np.float64)
+            if tg.shape != pts.shape:
+                raise ValueError("newton: target shape mismatch")
+        B = pts.shape[0]
+        out = np.empty_like(pts)
+        norms = np.empty((B, 2), np.float64)
+        status = np.empty(B, np.int32)
+        check(lib().pj_newton_host(self._h, _flags(precision, order), pts.ctypes.data,
+                                   tg.ctypes.data if tg is not None else None, B, iters, out.ctypes.data,
+                                   norms.ctypes.data, status.ctypes.data))
+        self._add_tally(B * iters)
+        return out, norms, status
+
+    @staticmethod
+    def _stream(stream, like):
+        if stream is None:
+            import torch
+            return torch.cuda.current_stream(like.device).cuda_stream
+        return stream.cuda_stream if hasattr(stream, "cuda_stream") else stream
+
+    def newton_solve_device(self, evals, points, out, precision: str = "dd", target=None, norms=None, status=None,
+                            stream=None) -> None:
+        """Asynchronous Newton solve from device-resident evaluator output (pj_newton_solve)."""
+        W = 2 if precision == "d" else 4
+        B = int(points.shape[0])
+        n = self.n
+        if tuple(points.shape) != (B, n, W) or tuple(out.shape) != (B, n, W) or \
+                tuple(evals.shape) != (B, n + n * n, W) or (target is not None and tuple(target.shape) != (B, n, W)):
+            raise ValueError("newton_solve_device: shape mismatch")
+        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        check(lib().pj_newton_solve(self._h, _flags(precision, None), evals.data_ptr(), points.data_ptr(), ptr(target),
+                                    B, out.data_ptr(), ptr(norms), ptr(status),
+                                    ctypes.c_void_p(self._stream(stream, points))))
+
+    def newton_step_device(self, points, work, out, precision: str = "dd", target=None, norms=None, status=None,
+                           order: str | None = None, stream=None) -> None:
+        """Asynchronous evaluate + Newton solve (pj_newton_step); work: [B, n + n*n, W]."""
+        W = 2 if precision == "d" else 4
+        B = int(points.shape[0])
+        n = self.n
+        if tuple(points.shape) != (B, n, W) or tuple(out.shape) != (B, n, W) or \
+                tuple(work.shape) != (B, n + n * n, W) or (target is not None and tuple(target.shape) != (B, n, W)):
+            raise ValueError("newton_step_device: shape mismatch")
+        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
+        check(lib().pj_newton_step(self._h, _flags(precision, order), points.data_ptr(), ptr(target), B,
+                                   work.data_ptr(), out.data_ptr(), ptr(norms), ptr(status),
+                                   ctypes.c_void_p(self._stream(stream, points))))
+
     # ---- index maps (bit-exact with the reference)
     def slot_targets(self, s: int) -> np.ndarray:
         out = np.empty(self.k + 1, np.int64)
