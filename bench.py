@@ -45,6 +45,18 @@ def model_flops(n, m, k, d, prec="dd"):
     return cmul * 80 + cadd * 40 if prec == "dd" else cmul * 6 + cadd * 2
 
 
+def newton_model_flops(n, prec="dd"):
+    """Cost model of one Newton solve (csrc/newton.cu), same weights as model_flops: per step kk the
+    R = n-kk-1 multipliers (cmul) and R*(n-kk) trailing updates (cmul + cadd, rhs column included);
+    n pivot inverses (counted as one cmul each); back substitution n cmul + n(n-1)/2 (cmul + cadd);
+    the final x + dx (n cadd)."""
+    R = [n - kk - 1 for kk in range(n)]
+    upd = sum(r * (r + 1) for r in R)
+    cmul = sum(R) + upd + n + n + n * (n - 1) // 2
+    cadd = upd + n * (n - 1) // 2 + n
+    return cmul * 80 + cadd * 40 if prec == "dd" else cmul * 6 + cadd * 2
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -210,6 +222,8 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--order", default="fast", choices=["fast", "ref"])
+    ap.add_argument("--no-extras", action="store_true",
+                    help="skip the secondary lines (C4 quality-up factor, f1 Newton step)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -354,6 +368,44 @@ def main():
         "clocks": clk,
     }
 
+    # ---------------- secondary measurements (outside the headline timed region)
+    if not args.no_extras:
+        def timed(fn, reps):
+            for _ in range(2):
+                fn()
+            stream.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                e0.record(stream)
+                for _ in range(reps):
+                    fn()
+                e1.record(stream)
+            stream.synchronize()
+            return e0.elapsed_time(e1) / reps
+        # C4: complex double vs complex double-double on the same points (quality-up overhead)
+        d2 = torch.from_numpy(np.stack([host_pts.real, host_pts.imag], -1).copy()).to(dev)
+        out_d = torch.empty((B, nout, 2), dtype=torch.float64, device=dev)
+        ms_d = timed(lambda: ctx.evaluate_device(d2, out_d, "d", None, stream), 10)
+        line["quality_up"] = {"config": "C4: C2 in complex double (reference order, bit-exact with the reference) "
+                                        "vs complex dd (fast order)",
+                              "d_evals_per_s": B / (ms_d * 1e-3), "dd_evals_per_s": B / (kern_ms * 1e-3),
+                              "dd_over_d_time": kern_ms / ms_d, "d_launch": ctx.launch("d")}
+        del out_d
+        # f1: one Newton step (evaluate + solve) per point on device, complex dd
+        xo = torch.empty_like(bufs[0])
+        nst = torch.empty(B, dtype=torch.int32, device=dev)
+        ms_solve = timed(lambda: ctx.newton_solve_device(out, bufs[0], xo, "dd", status=nst, stream=stream), 5)
+        ms_step = timed(lambda: ctx.newton_step_device(bufs[0], out, xo, "dd", status=nst, stream=stream), 5)
+        nf = newton_model_flops(N)
+        line["newton"] = {"config": "f1: C2 Newton step x <- x + J^-1 (-f), complex dd, 65,536 points per GPU",
+                          "steps_per_s": B / (ms_step * 1e-3), "ms_per_step": ms_step,
+                          "solve_ms": ms_solve, "solve_points_per_s": B / (ms_solve * 1e-3),
+                          "solve_flops_per_point": nf,
+                          "solve_fp64_frac": nf * B / (ms_solve * 1e-3) / 1e12 / peak,
+                          "status_ok_frac": float((nst == 0).float().mean().item()),
+                          "launch": ctx.launch("dd", newton=True)}
+        del xo
+
     # ---------------- CPU baseline (rank 0, N=1 only): the unmodified reference
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
@@ -376,6 +428,8 @@ def main():
                 got = ctx.evaluate_dd(p4[:chk])
                 err = np.maximum(np.abs((got[..., 0] - want[..., 0]) + (got[..., 1] - want[..., 1])),
                                  np.abs((got[..., 2] - want[..., 2]) + (got[..., 3] - want[..., 3])))
+                if "quality_up" in line:
+                    line["quality_up"]["cpu_dd_over_d_time"] = v / vdd  # reference (d) vs the dd restatement
                 line["parity_gate"] = {"points": chk, "max_err_over_sum_abs_terms": float(np.max(err / np.maximum(ms, 1e-300))),
                                        "tol": 1e-30}
         except Exception as exc:  # the baseline must never hide the measurement

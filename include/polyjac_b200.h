@@ -45,6 +45,7 @@ extern "C" {
 #define PJ_ORDER_REF 0x10   /* dd: keep the reference order in every stage (bit-exact with the
                                oracle's dd restatement); default dd order is the fast one */
 #define PJ_ORDER_FAST 0x20  /* d: allow the fast order (default for d is the reference order) */
+#define PJ_OP_NEWTON 0x100  /* pj_set_launch / pj_get_launch: address the Newton solve kernel */
 
 typedef struct pj_system_desc {
     int32_t n, m, k, d;
@@ -70,6 +71,13 @@ int pj_validate(const pj_system_desc* sys, char* msg, size_t cap);
  * build_layout, ref src/packing.cpp:19-52 (PJ_EINVAL for an invalid system or n > 256).
  * device < 0 creates a host-only context (packing and index maps, no evaluation). */
 int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out);
+/* Same, with options. PJ_CTX_WIDE lifts the reference's byte-encoding cap
+ * (build_layout rejects n > 256, ref src/packing.cpp:25-27): systems with n > 256 are packed with
+ * 32-bit position/exponent words (n <= 65535, k <= 2046) and evaluated by the generic kernel in
+ * every precision and order (same contracts as below). Without the option the reference's
+ * rejection is kept. */
+#define PJ_CTX_WIDE 0x1
+int pj_ctx_create_ex(const pj_system_desc* sys, int device, int options, pj_ctx** out);
 void pj_ctx_destroy(pj_ctx* ctx);
 
 /* Evaluate `batch` points already resident on the context's device; asynchronous on

@@ -11,8 +11,9 @@
 //     polyjac_b200::EvaluationContext ctx(sys);                       // was polyjac::EvaluationContext
 //     auto r = ctx.evaluate<polyjac::EvaluationResult>(point);        // bit-identical results
 //
-// B200 additions: complex double-double (evaluate_dd) and batched device-buffer evaluation on
-// a CUDA stream (evaluate_device).
+// B200 additions: complex double-double (evaluate_dd), batched device-buffer evaluation on a
+// CUDA stream (evaluate_device), the Newton corrector (newton, newton_dd, newton_step_device) and
+// the wide encoding for n > 256 (constructor option PJ_CTX_WIDE).
 #pragma once
 
 #include <chrono>
@@ -93,8 +94,10 @@ inline void check(int rc) {
 
 class EvaluationContext {
 public:
+    // options: PJ_CTX_WIDE lifts the reference's n <= 256 cap (pj_ctx_create_ex)
     template <class System>
-    explicit EvaluationContext(const System& sys, GridConfig grid = {}, int device = 0) : grid_(grid) {
+    explicit EvaluationContext(const System& sys, GridConfig grid = {}, int device = 0, int options = 0)
+        : grid_(grid) {
         if (grid_.block_size < 1) throw std::invalid_argument("block size must be >= 1");
         if (grid_.workers < 0) throw std::invalid_argument("workers must be >= 0");
         if (grid_.workers == 0) grid_.workers = 1;
@@ -118,7 +121,7 @@ public:
         }
         pj_system_desc desc{sys.n, sys.m, sys.k, sys.d, pos.data(), exps.data(), co.data()};
         if (!shape_ok) desc.positions = nullptr, desc.exponents = nullptr, desc.coeffs = nullptr;
-        detail::check(pj_ctx_create(&desc, device, &ctx_));
+        detail::check(pj_ctx_create_ex(&desc, device, options, &ctx_));
     }
     ~EvaluationContext() { pj_ctx_destroy(ctx_); }
     EvaluationContext(const EvaluationContext&) = delete;
@@ -182,6 +185,33 @@ public:
     // Device buffers, asynchronous on `stream` (cudaStream_t); flags = PJ_PREC_D | PJ_PREC_DD [| order].
     void evaluate_device(int flags, const double* d_points, std::int64_t batch, double* d_out, void* stream) {
         detail::check(pj_evaluate(ctx_, flags, d_points, batch, d_out, stream));
+        tally(batch);
+    }
+
+    // Newton corrector (B200 addition): `iters` steps x <- x + J(x)^-1 (y - f(x))
+    // per point on the GPU, host buffers [batch][n] (target y may be null: the roots of f).
+    // norms [batch][2] (|y - f|, |last step|) and status [batch] (0 ok, 1 singular, 2 non-finite)
+    // may be null.
+    void newton_dd(const ComplexDD* points, const ComplexDD* target, std::int64_t batch, int iters, ComplexDD* out,
+                   double* norms = nullptr, std::int32_t* status = nullptr) {
+        detail::check(pj_newton_host(ctx_, PJ_PREC_DD, reinterpret_cast<const double*>(points),
+                                     reinterpret_cast<const double*>(target), batch, iters,
+                                     reinterpret_cast<double*>(out), norms, status));
+        tally(batch * iters);
+    }
+    void newton(const Complex* points, const Complex* target, std::int64_t batch, int iters, Complex* out,
+                double* norms = nullptr, std::int32_t* status = nullptr) {
+        detail::check(pj_newton_host(ctx_, PJ_PREC_D, reinterpret_cast<const double*>(points),
+                                     reinterpret_cast<const double*>(target), batch, iters,
+                                     reinterpret_cast<double*>(out), norms, status));
+        tally(batch * iters);
+    }
+    // Device buffers: evaluate into d_work ([batch][n + n*n]) and solve, asynchronous on `stream`.
+    void newton_step_device(int flags, const double* d_points, const double* d_target, std::int64_t batch,
+                            double* d_work, double* d_points_out, double* d_norms, std::int32_t* d_status,
+                            void* stream) {
+        detail::check(pj_newton_step(ctx_, flags, d_points, d_target, batch, d_work, d_points_out, d_norms,
+                                     d_status, stream));
         tally(batch);
     }
 

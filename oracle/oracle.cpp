@@ -298,11 +298,12 @@ void evaluate_range(const System& S, const double* pts, long b0, long b1, double
 
 // ------------------------------------------------------------------ Newton corrector (f1)
 // Restates the operation order defined in paper_1201_0499_b200/csrc/newton.cu (the reference
-// has no Newton step): rhs = y + (-f); Gaussian elimination with partial pivoting
-// on |Re hi| + |Im hi| (first maximum, strictly positive); pivot inverse conj(a)/|a|^2;
-// multipliers l = A[i][kk] * inv (normalised product); trailing update
-// A[i][j] + (-(l * A[kk][j])) with the dd product left unnormalised; back substitution
-// dx_i = rhs_i * inv_i, rhs_r + (-(A[r][i] * dx_i)) for r < i (descending i); x + dx.
+// has no Newton step): rhs = y + (-f); Gaussian elimination with implicit partial
+// pivoting on |Re hi| + |Im hi| (maximum over the rows not yet pivoted, strictly positive, ties
+// to the smallest row index); pivot inverse conj(a)/|a|^2; multipliers l = A[i][kk] * inv
+// (normalised product); trailing update A[i][j] + (-(l * A[piv][j])) with the dd product left
+// unnormalised; back substitution dx_s = rhs[piv_s] * inv_s, then rhs[piv_t] + (-(A[piv_t][s] * dx_s))
+// for t < s (descending s); x + dx.
 // The dd pieces are restated from their published algorithms (Dekker product with FMA,
 // Newton-corrected reciprocal), independently of the device copy.
 static inline CDD cdd_mul_u(CDD a, CDD b) {  // product without the closing Fast2Sum
@@ -394,10 +395,13 @@ void newton_one(int n, const double* ev, const double* x, const double* y, doubl
     }
     if (norms) norms[0] = rn;
     auto at = [&](int i, int j) -> T& { return A[size_t(i) * ld + j]; };
+    // implicit pivoting: rows stay in place, piv[kk] records the pivot row of step kk
+    std::vector<int> piv(n), step(n, n);
     for (int kk = 0; kk < n; ++kk) {
         double best = 0.0;
         int bi = -1;
-        for (int i = kk; i < n; ++i) {
+        for (int i = 0; i < n; ++i) {  // ascending row index: ties go to the smallest
+            if (step[i] < kk) continue;
             const double mg = NT::mag1(at(i, kk));
             if (mg > best) {
                 best = mg;
@@ -410,31 +414,36 @@ void newton_one(int n, const double* ev, const double* x, const double* y, doubl
             if (status) *status = 1;
             return;
         }
-        if (bi != kk)
-            for (int j = kk; j <= n; ++j) std::swap(at(kk, j), at(bi, j));
-        inv[kk] = NT::inv(at(kk, kk));
-        for (int i = kk + 1; i < n; ++i) at(i, kk) = O::mul(at(i, kk), inv[kk]);
-        for (int i = kk + 1; i < n; ++i)
-            for (int j = kk + 1; j <= n; ++j) at(i, j) = O::add(at(i, j), NT::neg(NT::umul(at(i, kk), at(kk, j))));
+        piv[kk] = bi;
+        step[bi] = kk;
+        inv[kk] = NT::inv(at(bi, kk));
+        for (int i = 0; i < n; ++i) {
+            if (step[i] <= kk) continue;
+            const T l = O::mul(at(i, kk), inv[kk]);
+            at(i, kk) = l;
+            for (int j = kk + 1; j <= n; ++j) at(i, j) = O::add(at(i, j), NT::neg(NT::umul(l, at(bi, j))));
+        }
     }
-    std::vector<T> rhs(n);
-    for (int i = 0; i < n; ++i) rhs[i] = at(i, n);
-    for (int i = n - 1; i >= 0; --i) {
-        const T dx = O::mul(rhs[i], inv[i]);
-        rhs[i] = dx;
-        for (int r = 0; r < i; ++r) rhs[r] = O::add(rhs[r], NT::neg(NT::umul(at(r, i), dx)));
+    std::vector<T> dx(n);
+    for (int s = n - 1; s >= 0; --s) {
+        dx[s] = O::mul(at(piv[s], n), inv[s]);
+        for (int t = 0; t < s; ++t) {
+            T& r = at(piv[t], n);
+            r = O::add(r, NT::neg(NT::umul(at(piv[t], s), dx[s])));
+        }
     }
     double dn = 0.0;
     bool fin = true;
     for (int i = 0; i < n; ++i) {
-        const T xn = O::add(O::load(x + size_t(i) * W), rhs[i]);
+        const T xn = O::add(O::load(x + size_t(i) * W), dx[i]);
         O::store(xo + size_t(i) * W, xn);
-        dn = std::fmax(dn, NT::magmax(rhs[i]));
+        dn = std::fmax(dn, NT::magmax(dx[i]));
         fin = fin && NT::finite(xn);
     }
     if (norms) norms[1] = dn;
     if (status) *status = fin ? 0 : 2;
 }
+
 }  // namespace oracle
 
 extern "C" {

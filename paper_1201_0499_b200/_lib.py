@@ -15,6 +15,8 @@ SO_PATH = os.environ.get("PJ_LIB_PATH") or os.path.join(HERE, "libpolyjac_b200.s
 PJ_OK, PJ_EINVAL, PJ_ERANGE, PJ_ECUDA, PJ_ENOMEM, PJ_ENONFINITE, PJ_EFORMAT = 0, 1, 2, 3, 4, 5, 6
 PJ_PREC_D, PJ_PREC_DD = 1, 2
 PJ_ORDER_REF, PJ_ORDER_FAST = 0x10, 0x20
+PJ_OP_NEWTON = 0x100
+PJ_CTX_WIDE = 0x1
 
 EXPORTS = [
     "pj_last_error", "pj_version", "pj_validate", "pj_ctx_create", "pj_ctx_destroy", "pj_evaluate",
@@ -23,6 +25,7 @@ EXPORTS = [
     "pj_get_launch", "pj_fp64_peak_probe", "pj_random_points_range", "pj_set_kernel_variant",
     "pj_system_read_file", "pj_system_read_text", "pj_system_view", "pj_system_free", "pj_system_write_file",
     "pj_system_write_text", "pj_newton_solve", "pj_newton_step", "pj_newton_host",
+    "pj_ctx_create_ex",
 ]
 
 
@@ -56,6 +59,7 @@ def lib():
     L.pj_version.restype = ctypes.c_char_p
     L.pj_validate.argtypes = [ctypes.POINTER(SystemDesc), ctypes.c_char_p, ctypes.c_size_t]
     L.pj_ctx_create.argtypes = [ctypes.POINTER(SystemDesc), ctypes.c_int, ctypes.POINTER(vp)]
+    L.pj_ctx_create_ex.argtypes = [ctypes.POINTER(SystemDesc), ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
     L.pj_ctx_destroy.argtypes = [vp]
     L.pj_ctx_destroy.restype = None
     L.pj_evaluate.argtypes = [vp, ctypes.c_int, vp, i64, vp, vp]

@@ -122,6 +122,8 @@ struct pj_ctx {
     std::vector<int> gm_off;
     std::vector<uint16_t> gm_ent;
     uint16_t* d_posexp = nullptr;
+    uint32_t* d_posexp32 = nullptr;  // wide encoding (n > 256)
+    bool wide = false;
     int* d_gm_off = nullptr;
     uint16_t* d_gm_ent = nullptr;
     std::vector<uint32_t> sch, seg;  // fast-kernel stage-3 schedule (host copies)
@@ -147,7 +149,7 @@ struct pj_ctx {
     // Newton corrector (f1): launch shape per precision, global matrix slabs when the
     // augmented matrix exceeds shared memory, host-API staging buffers
     struct NewtonPlan {
-        int blocks = 0, threads = 0;
+        int blocks = 0, threads = 0, over_threads = 0;
         size_t smem = 0;
         bool gscr = false;
     } newton[2];
@@ -167,6 +169,7 @@ struct pj_ctx {
         S.chunks = chunks;
         S.kp = kp;
         S.posexp = d_posexp;
+        S.posexp32 = wide ? d_posexp32 : nullptr;
         S.coef = d_coef[pi];
         S.gm_off = d_gm_off;
         S.gm_ent = d_gm_ent;
@@ -191,6 +194,7 @@ void free_ctx(pj_ctx* c) {
     cudaGetDevice(&prev);
     cudaSetDevice(c->device);
     cudaFree(c->d_posexp);
+    cudaFree(c->d_posexp32);
     cudaFree(c->d_gm_off);
     cudaFree(c->d_gm_ent);
     cudaFree(c->d_sch);
@@ -259,7 +263,7 @@ int choose_launch(pj_ctx* c, int mode) {
             best.gscratch = nullptr;
         }
     };
-    if (mode == kModeDDFast && pjb::fast_supported(c->k) && M.over_variant >= 0) {
+    if (mode == kModeDDFast && !c->wide && pjb::fast_supported(c->k) && M.over_variant >= 0) {
         // smaller tiles measured faster for the fast kernel (finer grid-stride balance)
         // measured (tools/tune.py): 8-warp CTAs beat more, smaller CTAs at equal residency;
         // among tiles that keep the residency, the largest (<= 4) is marginally best
@@ -308,14 +312,60 @@ int choose_launch(pj_ctx* c, int mode) {
     return PJ_OK;
 }
 
-int check_desc(const pj_system_desc* sys) {
+constexpr int kWideMaxN = 65535;
+
+int check_desc(const pj_system_desc* sys, bool wide) {
     if (!sys) return fail(PJ_EINVAL, "null system descriptor");
     auto v = validate(*sys);
     if (!v.empty()) return fail(PJ_EINVAL, "build_layout: invalid system: " + v.front().describe());
-    if (sys->n > 256) return fail(PJ_EINVAL, "build_layout: n > 256 does not fit the byte encoding");
+    if (!wide && sys->n > 256) return fail(PJ_EINVAL, "build_layout: n > 256 does not fit the byte encoding");
+    // wide encoding: 16-bit positions; stage-3 entries j*32 + g stay 16-bit
+    if (wide && sys->n > kWideMaxN) return fail(PJ_EINVAL, "build_layout: n exceeds the wide encoding (65535)");
+    if (wide && sys->k > 2046) return fail(PJ_EINVAL, "build_layout: k exceeds the wide encoding (2046)");
     return PJ_OK;
 }
 
+}  // namespace
+
+// ------------------------------------------------------------------ Newton corrector (f1)
+namespace {
+int newton_plan(pj_ctx* c, int pi, pj_ctx::NewtonPlan** out) {
+    pj_ctx::NewtonPlan& P = c->newton[pi];
+    const int prec = pi + 1;
+    const size_t mb = pjb::newton_matrix_bytes(prec, c->n), ib = pjb::newton_int_bytes(c->n);
+    if (!P.blocks) {
+        // n <= 32: 128-thread CTAs (the kernel is compiled for at most 128 there, newton.cu)
+        P.threads = P.over_threads ? P.over_threads : (c->n <= 32 ? 128 : 256);
+        if (c->n <= 32) P.threads = std::min(P.threads, 128);
+        if (mb + ib <= c->smem_optin) {
+            const int nb = pjb::newton_blocks_per_sm(prec, c->n, P.threads, mb + ib);
+            if (nb > 0) {
+                P.smem = mb + ib;
+                P.blocks = nb * c->sms;
+                P.gscr = false;
+            }
+        }
+        if (!P.blocks) {  // augmented matrix beyond shared memory: per-CTA slabs in HBM (L2-resident)
+            const int nb = std::max(1, std::min(pjb::newton_blocks_per_sm(prec, c->n, P.threads, ib), 4));
+            P.smem = ib;
+            P.blocks = nb * c->sms;
+            P.gscr = true;
+        }
+    }
+    if (P.gscr) {
+        const size_t stride = (mb / sizeof(double) + 31) / 32 * 32;
+        const size_t need = stride * sizeof(double) * size_t(P.blocks);
+        if (need > c->nscratch_bytes) {
+            cudaFree(c->d_nscratch);
+            c->d_nscratch = nullptr;
+            c->nscratch_bytes = 0;
+            PJ_CUDA(cudaMalloc(&c->d_nscratch, need));
+            c->nscratch_bytes = need;
+        }
+    }
+    *out = &P;
+    return PJ_OK;
+}
 }  // namespace
 
 extern "C" {
@@ -338,11 +388,18 @@ int pj_validate(const pj_system_desc* sys, char* msg, size_t cap) {
 }
 
 int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
+    return pj_ctx_create_ex(sys, device, 0, out);
+}
+
+int pj_ctx_create_ex(const pj_system_desc* sys, int device, int options, pj_ctx** out) {
     if (!out) return fail(PJ_EINVAL, "null output pointer");
     *out = nullptr;
-    int rc = check_desc(sys);
+    if (options & ~PJ_CTX_WIDE) return fail(PJ_EINVAL, "unknown context option");
+    const bool wide = (options & PJ_CTX_WIDE) && sys && sys->n > 256;
+    int rc = check_desc(sys, options & PJ_CTX_WIDE);
     if (rc) return rc;
     pj_ctx* c = new pj_ctx();
+    c->wide = wide;
     c->device = device;
     c->n = sys->n;
     c->m = sys->m;
@@ -354,11 +411,17 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
     c->pos.assign(sys->positions, sys->positions + nm * k);
     c->exps.assign(sys->exponents, sys->exponents + nm * k);
 
-    // packing v2: fused position/exponent words (ref src/packing.cpp:40-44)
-    std::vector<uint16_t> posexp(nm * c->kp, 0);
+    // packing v2: fused position/exponent words (ref src/packing.cpp:40-44); the wide encoding
+    // (n > 256) widens them to pos | (exp-1) << 16 in 32 bits
+    std::vector<uint16_t> posexp(wide ? 0 : nm * c->kp, 0);
+    std::vector<uint32_t> posexp32(wide ? nm * c->kp : 0, 0);
     for (size_t s = 0; s < nm; ++s)
-        for (size_t j = 0; j < k; ++j)
-            posexp[s * c->kp + j] = uint16_t(c->pos[s * k + j] | ((c->exps[s * k + j] - 1) << 8));
+        for (size_t j = 0; j < k; ++j) {
+            if (wide)
+                posexp32[s * c->kp + j] = uint32_t(c->pos[s * k + j]) | (uint32_t(c->exps[s * k + j] - 1) << 16);
+            else
+                posexp[s * c->kp + j] = uint16_t(c->pos[s * k + j] | ((c->exps[s * k + j] - 1) << 8));
+        }
     // coefficient planes, derivative-major with the power rule folded in (ref src/packing.cpp:46-49):
     // double: a*c rounded per component, exactly as the reference; dd: exact.
     std::vector<double> cd((k + 1) * 2 * nm), cdd((k + 1) * 4 * nm);
@@ -420,8 +483,9 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
 
     // fast-kernel stage-3 schedule: per (p, c) the output-major, ascending-g list of staged terms
     // (value terms first, then Jacobian columns), cut into 32 equal runs (one per lane); a segment
-    // is a maximal piece of one output inside one run
-    {
+    // is a maximal piece of one output inside one run (byte encoding only: the wide encoding
+    // always runs the generic kernel)
+    if (!wide) {
         const int R = c->k + 1;
         c->nseg = n + 1 + 32;
         c->sch.assign(size_t(n) * C * R * 32, 0);
@@ -482,6 +546,7 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
     cudaDeviceProp prop;
     if ((e = cudaGetDeviceProperties(&prop, device)) ||
         (e = up((void**)&c->d_posexp, posexp.data(), posexp.size() * 2)) ||
+        (e = up((void**)&c->d_posexp32, posexp32.data(), posexp32.size() * 4)) ||
         (e = up((void**)&c->d_coef[0], cd.data(), cd.size() * 8)) ||
         (e = up((void**)&c->d_coef[1], cdd.data(), cdd.size() * 8)) ||
         (e = up((void**)&c->d_coefT, cddT.data(), cddT.size() * 8)) ||
@@ -807,6 +872,13 @@ int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points) {
     if (pi < 0) return fail(PJ_EINVAL, "unknown precision flag");
     if (threads < 0 || threads > 256 || threads % 32) return fail(PJ_EINVAL, "threads must be a multiple of 32 <= 256");
     if (tile_points < 0) return fail(PJ_EINVAL, "tile_points must be >= 0");
+    if (flags & PJ_OP_NEWTON) {
+        if (threads == 32) return fail(PJ_EINVAL, "newton: threads must be >= 64");
+        ctx->newton[pi].over_threads = threads;
+        ctx->newton[pi].blocks = 0;  // re-planned on the next solve
+        g_err.clear();
+        return PJ_OK;
+    }
     ModeState& M = ctx->mode[mode_of(flags)];
     M.over_threads = threads;
     M.over_tp = tile_points;
@@ -840,6 +912,23 @@ int pj_get_launch(pj_ctx* ctx, int flags, int32_t* threads, int32_t* tile_points
     if (!ctx) return fail(PJ_EINVAL, "null context");
     const int pi = prec_index(flags);
     if (pi < 0) return fail(PJ_EINVAL, "unknown precision flag");
+    if (flags & PJ_OP_NEWTON) {
+        if (ctx->host_only) return fail(PJ_EINVAL, "host-only context");
+        int prev = 0;
+        cudaGetDevice(&prev);
+        cudaSetDevice(ctx->device);
+        pj_ctx::NewtonPlan* P = nullptr;
+        int rc = newton_plan(ctx, pi, &P);
+        cudaSetDevice(prev);
+        if (rc) return rc;
+        if (threads) *threads = P->threads;
+        if (tile_points) *tile_points = 1;
+        if (blocks) *blocks = P->blocks;
+        if (smem_bytes) *smem_bytes = int64_t(P->smem);
+        if (variant) *variant = P->gscr ? 1 : 0;
+        g_err.clear();
+        return PJ_OK;
+    }
     const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
     if (threads) *threads = L.threads;
     if (tile_points) *tile_points = L.tp;
@@ -851,44 +940,6 @@ int pj_get_launch(pj_ctx* ctx, int flags, int32_t* threads, int32_t* tile_points
 }
 
 
-// ------------------------------------------------------------------ Newton corrector (f1)
-namespace {
-int newton_plan(pj_ctx* c, int pi, pj_ctx::NewtonPlan** out) {
-    pj_ctx::NewtonPlan& P = c->newton[pi];
-    const int prec = pi + 1;
-    const size_t mb = pjb::newton_matrix_bytes(prec, c->n);
-    if (!P.blocks) {
-        P.threads = 256;
-        if (mb <= c->smem_optin) {
-            const int nb = pjb::newton_blocks_per_sm(prec, c->n, P.threads, mb);
-            if (nb > 0) {
-                P.smem = mb;
-                P.blocks = nb * c->sms;
-                P.gscr = false;
-            }
-        }
-        if (!P.blocks) {  // augmented matrix beyond shared memory: per-CTA slabs in HBM (L2-resident)
-            const int nb = std::max(1, std::min(pjb::newton_blocks_per_sm(prec, c->n, P.threads, 0), 4));
-            P.smem = 0;
-            P.blocks = nb * c->sms;
-            P.gscr = true;
-        }
-    }
-    if (P.gscr) {
-        const size_t stride = (mb / sizeof(double) + 31) / 32 * 32;
-        const size_t need = stride * sizeof(double) * size_t(P.blocks);
-        if (need > c->nscratch_bytes) {
-            cudaFree(c->d_nscratch);
-            c->d_nscratch = nullptr;
-            c->nscratch_bytes = 0;
-            PJ_CUDA(cudaMalloc(&c->d_nscratch, need));
-            c->nscratch_bytes = need;
-        }
-    }
-    *out = &P;
-    return PJ_OK;
-}
-}  // namespace
 
 int pj_newton_solve(pj_ctx* ctx, int flags, const double* d_evals, const double* d_points, const double* d_target,
                     int64_t batch, double* d_points_out, double* d_norms, int32_t* d_status, void* stream) {
@@ -902,6 +953,7 @@ int pj_newton_solve(pj_ctx* ctx, int flags, const double* d_evals, const double*
     }
     if (!d_evals || !d_points || !d_points_out) return fail(PJ_EINVAL, "newton: null buffer");
     if (ctx->host_only) return fail(PJ_EINVAL, "newton: host-only context (created with device < 0)");
+    if (ctx->n > 256) return fail(PJ_EINVAL, "newton: n > 256 is not supported");
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != ctx->device) PJ_CUDA(cudaSetDevice(ctx->device));

@@ -93,13 +93,16 @@ __global__ void __launch_bounds__(256) eval_kernel(DevSystem S, const double* __
                 if (g < m) {
                     const int s = p * m + g;
                     const uint16_t* pe = S.posexp + (size_t)s * S.kp;
+                    const uint32_t* pe32 = S.posexp32 + (size_t)s * S.kp;
+                    const bool wide = S.posexp32 != nullptr;  // uniform across the grid
                     const double* cf = S.coef + s;
-                    auto X = [&](int j) -> T { return O::ld_planes(xt + (__ldg(pe + j) & 255), n); };
+                    auto POS = [&](int j) -> int { return wide ? int(__ldg(pe32 + j) & 0xffffu) : (__ldg(pe + j) & 255); };
+                    auto EXP = [&](int j) -> int { return wide ? int(__ldg(pe32 + j) >> 16) : (__ldg(pe + j) >> 8); };
+                    auto X = [&](int j) -> T { return O::ld_planes(xt + POS(j), n); };
                     auto PW = [&](int j) -> T {
-                        const int q = __ldg(pe + j);
-                        const int e = q >> 8;
+                        const int e = EXP(j);
                         if (e == 0) return O::one();
-                        return O::ld_planes(xt + (e - 1) * W * n + (q & 255), n);
+                        return O::ld_planes(xt + (e - 1) * W * n + POS(j), n);
                     };
                     auto COEF = [&](int j) -> T {
                         const double* q = cf + (size_t)j * W * nm;

@@ -16,6 +16,9 @@ struct DevSystem {
     // posexp[s*kp + j] = pos | (exp-1) << 8   (the reference's two byte arrays,
     // ref src/packing.cpp:40-44, fused into one 16-bit word per (s, j))
     const uint16_t* posexp;
+    // wide encoding (n > 256): posexp32[s*kp + j] = pos | (exp-1) << 16; null when
+    // the byte encoding is in use
+    const uint32_t* posexp32;
     // coefficient planes, derivative-major like ref src/packing.cpp:46-49:
     // component c of (j, s) at coef[(j*W + c)*nm + s]; block j < k = a_j*c, block k = c
     const double* coef;
@@ -78,7 +81,8 @@ struct NewtonArgs {
     double* gscratch;      // non-null: per-CTA matrix slabs in global memory (gstride doubles each)
     size_t gstride;
 };
-size_t newton_matrix_bytes(int prec, int n);
+size_t newton_matrix_bytes(int prec, int n);  // matrix planes, inverses, solution
+size_t newton_int_bytes(int n);               // pivot bookkeeping (always in shared memory)
 int newton_blocks_per_sm(int prec, int n, int threads, size_t smem);
 cudaError_t launch_newton(int prec, const NewtonArgs& args, int blocks, int threads, size_t smem, cudaStream_t st);
 

@@ -11,28 +11,32 @@
 // verbatim by the oracle (oracle/oracle.cpp: newton_one), which makes the device result
 // bit-identical to the oracle in both precisions.
 //
-// Operation order (T = complex double or complex double-double):
+// Operation order (T = complex double or complex double-double); pivoting is implicit (rows are
+// never moved, the pivot sequence is recorded), the arithmetic is that of the row-swapping form:
 //   rhs_i = y_i + (−f_i)                          (−f_i when y is absent)
-//   for kk = 0..n−1:
-//     piv = first i ≥ kk maximising |Re_hi A[i][kk]| + |Im_hi A[i][kk]| (strictly > 0, else
-//           the point is singular: status 1, x_new = x)
-//     swap rows kk, piv over columns kk..n (column n = rhs)
-//     inv_kk = 1 / A[kk][kk]                       (cinv below)
-//     l_i = A[i][kk] · inv_kk                     i > kk (normalised product)
-//     A[i][j] = A[i][j] + (−(l_i · A[kk][j]))     i > kk, j = kk+1..n (dd: product left
-//                                                  unnormalised, the addition renormalises)
-//   for i = n−1..0:  dx_i = rhs_i · inv_i;  rhs_r = rhs_r + (−(A[r][i] · dx_i))  for r < i
+//   active rows: all; for kk = 0..n−1:
+//     piv_kk = the active row maximising |Re_hi A[i][kk]| + |Im_hi A[i][kk]| (ties: the smallest
+//              row index; the maximum must be > 0, else the point is singular: status 1, x_new = x)
+//     inv_kk = 1 / A[piv_kk][kk]                   (conj(a) / |a|², nt_inv below); piv_kk leaves
+//              the active set
+//     l_i = A[i][kk] · inv_kk                      active i (normalised product)
+//     A[i][j] = A[i][j] + (−(l_i · A[piv_kk][j]))  active i, j = kk+1..n (column n = rhs; the dd
+//                                                  product is left unnormalised, the addition
+//                                                  renormalises)
+//   for s = n−1..0:  dx_s = rhs[piv_s] · inv_s;  rhs[piv_t] = rhs[piv_t] + (−(A[piv_t][s] · dx_s)) for t < s
 //   x_new_i = x_i + dx_i
 //
 // B200 mapping: a CTA owns one point at a time (persistent grid over the batch). The
 // augmented matrix [J | rhs] lives in shared memory as W planes of n × (n+1) doubles (row
-// stride n+1: a warp's column walk hits every bank pair once); n ≤ 64 fits (133 KB in dd), larger
-// systems use a per-CTA global scratch slab with the same code. Warp 0 does the pivot search
-// (shuffle arg-max), the row swap, the pivot inverse and the multipliers; all warps then
-// update the trailing block (one element per thread per pass); back substitution runs in warp
-// 0 with the right-hand side in registers (a lane owns rows lane + 32q) and the solved
-// component broadcast by shuffle. Several CTAs per SM overlap one CTA's serial phases with the
-// others' trailing updates. The path is FP64-issue-bound like the evaluator.
+// stride n+1); n ≤ 64 fits (133 KB in dd), larger systems use a per-CTA global slab with the
+// same code. Warp 0 runs one column ahead ("look-ahead"): during step kk it updates column
+// kk+1 of the active rows (the values stay in its registers), picks piv_{kk+1} by a shuffle
+// arg-max, forms the pivot inverse and the multipliers of column kk+1 and the next active-row
+// list — while warps 1.. update columns kk+2..n of step kk (a thread keeps one pivot-row element
+// in registers and walks rows). One barrier per step. Back substitution runs in warp 0 with the
+// right-hand side in registers (a lane owns rows lane + 32q) and each solved component
+// broadcast by shuffle. Several CTAs per SM overlap one CTA's serial phases with the others'
+// updates. The path is FP64-issue-bound like the evaluator.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -88,6 +92,9 @@ __device__ __forceinline__ CDD nt_inv(CDD a) {
     return {o.hi, o.lo, p.hi, p.lo};
 }
 
+// dynamic shared memory ints (4 per row), rounded to whole 16-byte units, in doubles
+__host__ __device__ __forceinline__ int newton_int_words(int n) { return (4 * n + 3) / 4 * 2; }
+
 template <class T>
 __device__ __forceinline__ T shfl_idx(T v, int src);
 template <>
@@ -100,19 +107,91 @@ __device__ __forceinline__ CDD shfl_idx<CDD>(CDD v, int src) {
             __shfl_sync(0xffffffffu, v.ih, src), __shfl_sync(0xffffffffu, v.il, src)};
 }
 
-// NQ: rows per lane in back substitution (n <= 32*NQ)
+// NQ: active-row slots per lane (look-ahead) and rows per lane (back substitution), n <= 32*NQ
+// kRecip[c] = ceil(2^16 / c): floor(x / c) == (x * kRecip[c]) >> 16 for x, c <= 256
+__constant__ unsigned kRecip[257];
+// rows per update pass of an updater thread (measured at C2: 1 beats 2 and 4 — registers)
+constexpr int kUnroll = 1;
+
+// n <= 32 (NQ = 1) runs 128-thread CTAs, six per SM (the matrix is 36 KB in dd): 85 registers
+template <int NQ>
+struct NtBounds {
+    static constexpr int threads = NQ == 1 ? 128 : 256, blocks = NQ == 1 ? 6 : 1;
+};
 template <class T, int NQ>
-__global__ void __launch_bounds__(256) newton_kernel(NewtonArgs a) {
+__global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) newton_kernel(NewtonArgs a) {
     using S = Sc<T>;
     constexpr int W = S::W;
     extern __shared__ __align__(16) double smem[];
-    __shared__ int s_piv;
+    __shared__ int s_sing;
     const int n = a.n, ld = n + 1, P = n * ld;
     const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
-    double* A = a.gscratch ? a.gscratch + size_t(blockIdx.x) * a.gstride : smem;
+    // dynamic shared memory: ints (pivot rows, pivot step of each row, two active-row lists), then
+    // the matrix planes unless they live in a global slab
+    int* s_piv = reinterpret_cast<int*>(smem);
+    int* s_step = s_piv + n;
+    int* s_list0 = s_step + n;
+    int* s_list1 = s_list0 + n;
+    double* A = a.gscratch ? a.gscratch + size_t(blockIdx.x) * a.gstride : smem + newton_int_words(n);
     double* INV = A + size_t(W) * P;  // [W][n] pivot inverses
+    double* DX = INV + size_t(W) * n;   // [W][n] solution
     const size_t nout = size_t(n) * n + n;
 
+    // Warp-0 look-ahead for column c: rows list[0..R) (values v[] already in registers), pick the
+    // pivot, store inv_c and the multipliers of column c, write the next list (R-1 rows).
+    auto pivot_phase = [&](int c, const int* list, int R, const T* v, int* next) {
+        double best = 0.0;
+        int bi = -1, bq = 0;
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int idx = lane + 32 * q;
+            if (idx < R) {
+                const double mg = nt_mag1(v[q]);
+                const int r = list[idx];
+                if (mg > best || (mg == best && bi >= 0 && r < bi)) {
+                    best = mg;
+                    bi = r;
+                    bq = idx;
+                }
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+            if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) {
+                best = ob;
+                bi = oi;
+                bq = oq;
+            }
+        }
+        if (bi < 0) {
+            if (lane == 0) s_sing = 1;
+            return;
+        }
+        // broadcast the pivot value from its owner, every lane forms the same inverse
+        T pv = v[0];
+#pragma unroll
+        for (int q = 1; q < NQ; ++q)
+            if (q == (bq >> 5)) pv = v[q];
+        pv = shfl_idx(pv, bq & 31);
+        const T iv = nt_inv(pv);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) {
+            const int idx = lane + 32 * q;
+            if (idx < R) {
+                const int r = list[idx];
+                if (r != bi) S::st_planes(A + r * ld + c, P, S::mul(v[q], iv));
+                // next list: the pivot's slot takes the last row
+                if (idx < R - 1) next[idx] = idx == bq ? list[R - 1] : r;
+            }
+        }
+        if (lane == 0) {
+            S::st_planes(INV + c, n, iv);
+            s_piv[c] = bi;
+            s_step[bi] = c;
+        }
+    };
     for (long long b = blockIdx.x; b < a.B; b += gridDim.x) {
         const double* ev = a.evals + size_t(b) * nout * W;
         // ---- load [J | y − f] into planes
@@ -127,66 +206,88 @@ __global__ void __launch_bounds__(256) newton_kernel(NewtonArgs a) {
                 if (a.target) r = S::add(S::ld_aos(a.target + (size_t(b) * n + i) * W), r);
                 S::st_planes(A + i * ld + n, P, r);
                 rn = fmax(rn, nt_magmax(r));
+                s_list0[i] = i;
             }
             for (int o = 16; o; o >>= 1) rn = fmax(rn, __shfl_xor_sync(0xffffffffu, rn, o));
-            if (lane == 0 && a.norms) a.norms[2 * b] = rn;
+            if (lane == 0) {
+                if (a.norms) a.norms[2 * b] = rn;
+                s_sing = 0;
+            }
+        }
+        __syncthreads();
+        // ---- column 0: pivot, inverse, multipliers
+        if (warp == 0) {
+            T v[NQ];
+#pragma unroll
+            for (int q = 0; q < NQ; ++q) {
+                const int idx = lane + 32 * q;
+                v[q] = idx < n ? S::ld_planes(A + idx * ld, P) : S::zero();
+            }
+            pivot_phase(0, s_list0, n, v, s_list1);
         }
         __syncthreads();
 
-        // ---- elimination with partial pivoting
-        bool singular = false;
-        for (int kk = 0; kk < n; ++kk) {
+        // ---- elimination: step kk updates the active rows (R of them) at columns kk+1..n; warp 0
+        // takes column kk+1 and looks ahead, warps 1.. the rest.
+        bool singular = s_sing != 0;
+        for (int kk = 0; kk < n && !singular; ++kk) {
+            const int R = n - kk - 1;
+            const int* list = (kk & 1) ? s_list0 : s_list1;
+            int* next = (kk & 1) ? s_list1 : s_list0;
+            const int pr = s_piv[kk];
             if (warp == 0) {
-                double best = 0.0;
-                int bi = -1;
-                for (int i = kk + lane; i < n; i += 32) {
-                    const double mg = nt_mag1(S::ld_planes(A + i * ld + kk, P));
-                    if (mg > best) {
-                        best = mg;
-                        bi = i;
-                    }
-                }
-                for (int o = 16; o; o >>= 1) {
-                    const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-                    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-                    if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) {
-                        best = ob;
-                        bi = oi;
-                    }
-                }
-                if (bi >= 0) {
-                    if (bi != kk)
-                        for (int j = kk + lane; j <= n; j += 32) {
-                            T u = S::ld_planes(A + kk * ld + j, P), v = S::ld_planes(A + bi * ld + j, P);
-                            S::st_planes(A + kk * ld + j, P, v);
-                            S::st_planes(A + bi * ld + j, P, u);
+                if (kk + 1 < n) {
+                    const int c = kk + 1;
+                    const T u = S::ld_planes(A + pr * ld + c, P);
+                    T v[NQ];
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) {
+                        const int idx = lane + 32 * q;
+                        if (idx < R) {
+                            const int r = list[idx];
+                            v[q] = S::add(S::ld_planes(A + r * ld + c, P),
+                                          nt_neg(nt_umul(S::ld_planes(A + r * ld + kk, P), u)));
+                        } else {
+                            v[q] = S::zero();
                         }
-                    __syncwarp();
-                    const T iv = nt_inv(S::ld_planes(A + kk * ld + kk, P));  // every lane, same value
-                    if (lane == 0) S::st_planes(INV + kk, n, iv);
-                    for (int i = kk + 1 + lane; i < n; i += 32)
-                        S::st_planes(A + i * ld + kk, P, S::mul(S::ld_planes(A + i * ld + kk, P), iv));
+                    }
+                    pivot_phase(c, list, R, v, next);
                 }
-                if (lane == 0) s_piv = bi;
+            } else {
+                // columns kk+2..n (Cp of them) for R rows: a thread keeps u = A[pr][j] in registers
+                // and walks rows rg, rg+G, ... (kUnroll rows per pass, loads before stores)
+                const int Cp = n - kk - 1, Tp = nt - 32, tp = tid - 32;
+                for (int c0 = 0; c0 < Cp; c0 += Tp) {
+                    const int cw = min(Tp, Cp - c0);
+                    const unsigned rc = kRecip[cw];
+                    const int G = int((unsigned(Tp) * rc) >> 16), rg = int((unsigned(tp) * rc) >> 16);
+                    if (rg >= G) continue;
+                    const int j = kk + 2 + c0 + (tp - rg * cw);
+                    const T u = S::ld_planes(A + pr * ld + j, P);
+                    for (int idx = rg; idx < R; idx += kUnroll * G) {
+                        T l[kUnroll], v[kUnroll];
+                        int rows[kUnroll];
+#pragma unroll
+                        for (int e = 0; e < kUnroll; ++e) {
+                            const int ix = idx + e * G;
+                            rows[e] = ix < R ? list[ix] : -1;
+                            if (rows[e] >= 0) {
+                                l[e] = S::ld_planes(A + rows[e] * ld + kk, P);
+                                v[e] = S::ld_planes(A + rows[e] * ld + j, P);
+                            }
+                        }
+#pragma unroll
+                        for (int e = 0; e < kUnroll; ++e)
+                            if (rows[e] >= 0) S::st_planes(A + rows[e] * ld + j, P, S::add(v[e], nt_neg(nt_umul(l[e], u))));
+                    }
+                }
             }
             __syncthreads();
-            if (s_piv < 0) {
-                singular = true;
-                break;
-            }
-            const int R = n - kk - 1, C = n - kk;
-            for (int e = tid; e < R * C; e += nt) {
-                const int r = e / C;
-                const int i = kk + 1 + r, j = kk + 1 + (e - r * C);
-                const T l = S::ld_planes(A + i * ld + kk, P);
-                const T u = S::ld_planes(A + kk * ld + j, P);
-                const T v = S::ld_planes(A + i * ld + j, P);
-                S::st_planes(A + i * ld + j, P, S::add(v, nt_neg(nt_umul(l, u))));
-            }
-            __syncthreads();
+            singular = s_sing != 0;
         }
 
-        // ---- back substitution (warp 0), rhs rows lane + 32q in registers
+        // ---- back substitution (warp 0): rhs of physical rows lane + 32q in registers;
+        // dx_s = rhs[piv_s] * inv_s, then rhs[piv_t] -= A[piv_t][s] * dx_s for t < s
         if (warp == 0) {
             const double* x = a.points + size_t(b) * n * W;
             double* xo = a.points_out + size_t(b) * n * W;
@@ -198,37 +299,37 @@ __global__ void __launch_bounds__(256) newton_kernel(NewtonArgs a) {
                 }
             } else {
                 T rr[NQ];
+                int st[NQ];
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) {
                     const int r = lane + 32 * q;
                     rr[q] = r < n ? S::ld_planes(A + r * ld + n, P) : S::zero();
+                    st[q] = r < n ? s_step[r] : -1;
                 }
-                for (int i = n - 1; i >= 0; --i) {
-                    const int owner = i & 31, qi = i >> 5;
-                    T v = rr[0];
+                for (int s = n - 1; s >= 0; --s) {
+                    const int pr = s_piv[s];
+                    const int owner = pr & 31, qi = pr >> 5;
+                    T xs = rr[0];
 #pragma unroll
                     for (int q = 1; q < NQ; ++q)
-                        if (q == qi) v = rr[q];
-                    v = shfl_idx(v, owner);
-                    const T dx = S::mul(v, S::ld_planes(INV + i, n));
+                        if (q == qi) xs = rr[q];
+                    xs = shfl_idx(xs, owner);
+                    xs = S::mul(xs, S::ld_planes(INV + s, n));
+                    if (lane == 0) S::st_planes(DX + s, n, xs);
 #pragma unroll
-                    for (int q = 0; q < NQ; ++q) {
-                        const int r = lane + 32 * q;
-                        if (r < i) rr[q] = S::add(rr[q], nt_neg(nt_umul(S::ld_planes(A + r * ld + i, P), dx)));
-                        if (r == i) rr[q] = dx;
-                    }
+                    for (int q = 0; q < NQ; ++q)
+                        if (st[q] >= 0 && st[q] < s)
+                            rr[q] = S::add(rr[q], nt_neg(nt_umul(S::ld_planes(A + (lane + 32 * q) * ld + s, P), xs)));
                 }
+                __syncwarp();
                 double dn = 0.0;
                 bool fin = true;
-#pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    const int r = lane + 32 * q;
-                    if (r < n) {
-                        const T xn = S::add(S::ld_aos(x + size_t(r) * W), rr[q]);
-                        S::st_aos(xo + size_t(r) * W, xn);
-                        dn = fmax(dn, nt_magmax(rr[q]));
-                        fin = fin && nt_finite(xn);
-                    }
+                for (int i = lane; i < n; i += 32) {
+                    const T d = S::ld_planes(DX + i, n);
+                    const T xn = S::add(S::ld_aos(x + size_t(i) * W), d);
+                    S::st_aos(xo + size_t(i) * W, xn);
+                    dn = fmax(dn, nt_magmax(d));
+                    fin = fin && nt_finite(xn);
                 }
                 for (int o = 16; o; o >>= 1) dn = fmax(dn, __shfl_xor_sync(0xffffffffu, dn, o));
                 fin = __all_sync(0xffffffffu, fin);
@@ -258,7 +359,19 @@ const void* fn_of(int prec, int n) { return prec == 1 ? newton_fn<CD>(nq_of(n)) 
 
 size_t newton_matrix_bytes(int prec, int n) {
     const int W = prec == 1 ? 2 : 4;
-    return (size_t(W) * n * (n + 1) + size_t(W) * n) * sizeof(double);
+    return (size_t(W) * n * (n + 1) + 2 * size_t(W) * n) * sizeof(double);
+}
+size_t newton_int_bytes(int n) { return size_t(newton_int_words(n)) * sizeof(double); }
+
+static cudaError_t init_recip() {
+    static bool done = false;
+    if (done) return cudaSuccess;
+    unsigned h[257];
+    h[0] = 0;
+    for (int c = 1; c <= 256; ++c) h[c] = (65536u + c - 1) / c;
+    cudaError_t e = cudaMemcpyToSymbol(kRecip, h, sizeof(h));
+    if (e == cudaSuccess) done = true;
+    return e;
 }
 
 int newton_blocks_per_sm(int prec, int n, int threads, size_t smem) {
@@ -272,6 +385,7 @@ int newton_blocks_per_sm(int prec, int n, int threads, size_t smem) {
 cudaError_t launch_newton(int prec, const NewtonArgs& args, int blocks, int threads, size_t smem, cudaStream_t st) {
     if (args.B <= 0) return cudaSuccess;
     const void* f = fn_of(prec, args.n);
+    if (cudaError_t e = init_recip()) return e;
     if (smem) {
         cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         if (e) return e;

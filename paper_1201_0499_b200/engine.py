@@ -279,7 +279,8 @@ class EvaluationContext:
     Like the reference, one context must not serve concurrent evaluate calls; use one per
     thread (or per device / stream)."""
 
-    def __init__(self, sys: PolynomialSystem, grid: GridConfig | None = None, device: int = 0):
+    def __init__(self, sys: PolynomialSystem, grid: GridConfig | None = None, device: int = 0, wide: bool = False):
+        """wide=True lifts the reference's n <= 256 byte-encoding cap (pj_ctx_create_ex, PJ_CTX_WIDE)."""
         grid = grid or GridConfig()
         if grid.block_size < 1:
             raise ValueError("block size must be >= 1")
@@ -290,7 +291,7 @@ class EvaluationContext:
         self.device = device
         desc, keep = sys._desc()
         h = ctypes.c_void_p()
-        check(lib().pj_ctx_create(ctypes.byref(desc), device, ctypes.byref(h)))
+        check(lib().pj_ctx_create_ex(ctypes.byref(desc), device, _lib.PJ_CTX_WIDE if wide else 0, ctypes.byref(h)))
         self._h = h
         self._mults = MultCounter()
 
@@ -497,17 +498,21 @@ class EvaluationContext:
         return out
 
     # ---- launch shape
-    def set_launch(self, precision: str, threads: int = 0, tile_points: int = 0, order: str | None = None) -> None:
-        check(lib().pj_set_launch(self._h, _flags(precision, order), threads, tile_points))
+    def set_launch(self, precision: str, threads: int = 0, tile_points: int = 0, order: str | None = None,
+                   newton: bool = False) -> None:
+        """Override the launch shape of the evaluation kernel (or, newton=True, the Newton solve)."""
+        f = _flags(precision, order) | (_lib.PJ_OP_NEWTON if newton else 0)
+        check(lib().pj_set_launch(self._h, f, threads, tile_points))
 
     def set_variant(self, variant: int) -> None:
         """Kernel variant of the fast dd order (see pj_set_kernel_variant): 0 auto, -1 generic."""
         check(lib().pj_set_kernel_variant(self._h, _flags("dd", None), variant))
 
-    def launch(self, precision: str, order: str | None = None):
+    def launch(self, precision: str, order: str | None = None, newton: bool = False):
         t, tp, b, var = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         sm = ctypes.c_int64()
-        check(lib().pj_get_launch(self._h, _flags(precision, order), ctypes.byref(t), ctypes.byref(tp),
+        f = _flags(precision, order) | (_lib.PJ_OP_NEWTON if newton else 0)
+        check(lib().pj_get_launch(self._h, f, ctypes.byref(t), ctypes.byref(tp),
                                   ctypes.byref(b), ctypes.byref(sm), ctypes.byref(var)))
         return dict(threads=t.value, tile_points=tp.value, blocks=b.value, smem_bytes=sm.value, variant=var.value)
 

@@ -93,6 +93,16 @@ int main() {
         PolynomialSystem wide{300, 1, 1, 1, {}};
         for (int p = 0; p < 300; ++p) wide.terms.push_back({{1.0, 0.0}, {{p}, {1}}});
         CHECK(throws<std::invalid_argument>([&] { polyjac_b200::EvaluationContext c(wide); }));
+        {  // the wide encoding accepts it (B200 addition) and evaluates f_p = x_p exactly
+            polyjac_b200::EvaluationContext c(wide, {}, 0, PJ_CTX_WIDE);
+            EvaluationPoint x(300);
+            for (int i = 0; i < 300; ++i) x[i] = {0.5 + i, -1.0 * i};
+            const auto r = c.evaluate<EvaluationResult>(x);
+            bool ok = true;
+            for (int i = 0; i < 300; ++i)
+                ok = ok && r.values[i].re == x[i].re && r.values[i].im == x[i].im && r.jac(i, i).re == 1.0;
+            CHECK(ok);
+        }
         PolynomialSystem shortsys = sys;
         shortsys.terms.pop_back();
         CHECK(throws<std::invalid_argument>([&] { polyjac_b200::EvaluationContext c(shortsys); }));
@@ -112,6 +122,26 @@ int main() {
         CHECK(out[0].re_hi == 15 && out[2].re_hi == 5 && out[3].re_hi == 3);
         auto r = ctx.evaluate<EvaluationResult>(EvaluationPoint{{3.0, 0.0}, {5.0, 0.0}});
         CHECK(compare(r, sys, {{3.0, 0.0}, {5.0, 0.0}}, 1e-10).pass);
+    }
+    // Newton corrector (B200 addition): f_p = x_{(p+1) mod 3} has J a permutation, one step lands
+    // exactly on the root; a variable in no monomial makes J singular (status 1, x unchanged)
+    {
+        PolynomialSystem sys{3, 1, 1, 1, {}};
+        for (int p = 0; p < 3; ++p) sys.terms.push_back({{1.0, 0.0}, {{(p + 1) % 3}, {1}}});
+        polyjac_b200::EvaluationContext ctx(sys);
+        polyjac_b200::ComplexDD x[3] = {{0.25, 1e-20, -0.5, 0}, {0.75, 0, 0.125, -1e-21}, {-0.3, 0, 0.9, 0}};
+        polyjac_b200::ComplexDD xo[3];
+        double norms[2];
+        std::int32_t st = -1;
+        ctx.newton_dd(x, nullptr, 1, 1, xo, norms, &st);
+        CHECK(st == 0 && norms[0] == 0.9);
+        for (const auto& v : xo) CHECK(v.re_hi == 0 && v.re_lo == 0 && v.im_hi == 0 && v.im_lo == 0);
+        PolynomialSystem sing{2, 1, 1, 1, {}};
+        sing.terms = {{{1.0, 0.0}, {{0}, {1}}}, {{2.0, 0.0}, {{0}, {1}}}};
+        polyjac_b200::EvaluationContext c2(sing);
+        polyjac_b200::Complex y[2] = {{0.5, 0.0}, {0.25, 0.0}}, yo[2];
+        c2.newton(y, nullptr, 1, 2, yo, norms, &st);
+        CHECK(st == 1 && yo[0].re == 0.5 && yo[1].re == 0.25);
     }
     std::printf("%s: %d passed, %d failed\n", g_fail ? "FAIL" : "PASS", g_pass, g_fail);
     return g_fail ? 1 : 0;

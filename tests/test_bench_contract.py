@@ -28,3 +28,11 @@ def test_model_flops_matches_survey():
     assert bench.model_flops(32, 32, 8, 2) == 3891200
     assert bench.model_flops(64, 64, 16, 10) == 32645120   # C3
     assert bench.model_flops(32, 32, 8, 2, "d") == 282624
+
+
+def test_newton_model_flops():
+    sys.path.insert(0, ROOT)
+    import bench
+    # n = 32: 11,968 complex products and 11,440 complex additions per solve (docstring of the model)
+    assert bench.newton_model_flops(32) == 11968 * 80 + 11440 * 40
+    assert bench.newton_model_flops(1) == 2 * 80 + 1 * 40  # one inverse, one dx product, x + dx

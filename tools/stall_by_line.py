@@ -1,5 +1,5 @@
 """Per-source-line stall breakdown (long_sb / short_sb / wait / math) from an ncu SASS source dump.
-usage: python tools/stall_by_line.py <nvdisasm -gi> <kernel> <sass csv> [top]"""
+usage: python tools/stall_by_line.py <nvdisasm -gi> <kernel> <sass csv> [top] [source-file substring]"""
 import csv
 import re
 import sys
@@ -7,6 +7,7 @@ from collections import defaultdict
 
 dis, kern, src = sys.argv[1:4]
 top = int(sys.argv[4]) if len(sys.argv) > 4 else 25
+srcpat = sys.argv[5] if len(sys.argv) > 5 else "eval_fast"
 off2line, cur, inside = {}, None, False
 for ln in open(dis):
     if ln.startswith("//----") and ".text." in ln:
@@ -17,14 +18,15 @@ for ln in open(dis):
     m = re.search(r'//## File "([^"]+)", line (\d+)(.*)', ln)
     if m:
         chain = [(m.group(1), int(m.group(2)))] + [(a, int(b)) for a, b in re.findall(r'inlined at "([^"]+)", line (\d+)', m.group(3))]
-        cur = next(((a, b) for a, b in chain if "eval_fast" in a), chain[-1])
+        cur = next(((a, b) for a, b in chain if srcpat in a), chain[-1])
         continue
     m = re.match(r'\s+/\*([0-9a-f]{4,})\*/', ln)
     if m and cur:
         off2line[int(m.group(1), 16)] = cur
 rows = list(csv.reader(open(src)))
 h = rows[1]
-cols = ["stall_long_sb", "stall_short_sb", "stall_wait", "stall_math", "stall_mio", "stall_branch_resolving"]
+cols = ["stall_long_sb", "stall_short_sb", "stall_wait", "stall_math", "stall_barrier", "stall_mio",
+        "stall_branch_resolving", "Instructions Executed"]
 idx = [h.index(c) for c in cols]
 ia = h.index("Address")
 agg = defaultdict(lambda: [0.0] * len(cols))
@@ -40,9 +42,10 @@ for r in rows[2:]:
         v = float(r[c] or 0)
         agg[k][i] += v
         tot[i] += v
-src_lines = {i: t.strip() for i, t in enumerate(open([f for f, _ in off2line.values() if "eval_fast" in f][0]), 1)}
+src_lines = {i: t.strip() for i, t in enumerate(open([f for f, _ in off2line.values() if srcpat in f][0]), 1)}
 print("totals:", {c: int(t) for c, t in zip(cols, tot)})
-for ci, c in enumerate(cols[:4]):
+for ci, c in enumerate(cols[:5] + cols[-1:]):
+    ci = cols.index(c)
     print(f"--- {c}")
-    for k in sorted(agg, key=lambda k: -agg[k][ci])[:6]:
+    for k in sorted(agg, key=lambda k: -agg[k][ci])[:top]:
         print(f"  {k:4d} {100 * agg[k][ci] / max(tot[ci], 1):5.1f}%  {src_lines.get(k, '')[:90]}")
