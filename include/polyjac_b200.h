@@ -166,13 +166,13 @@ int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double*
 /* Advanced: override the launch shape for `flags`' precision (threads per CTA, multiple of 32,
  * <= 256; points per CTA tile). 0 restores the automatic choice. */
 int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points);
-/* Advanced: kernel variant of the fast dd order. 0 = automatic, -1 = the generic kernel,
- * else (P << 2) | (FREG << 1) | SH: P in {1, 2} points per lane, SH = coordinates in registers
- * with warp-shuffle gathers (needs n <= 32, d <= 2), FREG = forward products in registers
- * (SH only). Results of every variant satisfy the same contract. */
+/* Advanced: kernel choice for complex double (PJ_PREC_D) or the fast dd order. 0 = automatic,
+ * -1 = the generic kernel (eval_kernels.cu), 1 = the k-specialised kernel (eval_fastd.cu for complex
+ * double, eval_fast.cu for dd). Every choice satisfies the same contract (complex double:
+ * bit-exact with the reference). */
 int pj_set_kernel_variant(pj_ctx* ctx, int flags, int variant);
 /* Report the launch shape used for `flags`: threads, tile points, blocks, dynamic smem bytes,
- * kernel variant (-1 = generic kernel). */
+ * kernel (-1 = generic, 1 = fast dd, 2 = fast complex double). */
 int pj_get_launch(pj_ctx* ctx, int flags, int32_t* threads, int32_t* tile_points, int32_t* blocks,
                   int64_t* smem_bytes, int32_t* variant);
 

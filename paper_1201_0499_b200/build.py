@@ -19,7 +19,7 @@ CLI = os.path.join(HERE, "polyjac_b200")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU = ["eval_kernels.cu", "eval_fast.cu", "newton.cu", "fp64_probe.cu"]
+CU = ["eval_kernels.cu", "eval_fast.cu", "eval_fastd.cu", "newton.cu", "fp64_probe.cu"]
 CPP = ["capi.cpp", "sysio.cpp"]
 HEADERS = ["dd.cuh", "eval_kernels.h"]
 

@@ -279,6 +279,18 @@ int choose_launch(pj_ctx* c, int mode) {
                 consider(1, nw, tp, sm, pjb::fast_blocks_per_sm(c->k, c->n, c->d, nw * 32, sm), int(ftps.size() - i));
             }
     }
+    if (mode == kModeD && !c->wide && pjb::fastd_supported(c->k) && M.over_variant >= 0) {
+        // point pairs per warp: tiles of 2 points per warp (one pair task per warp per row sweep)
+        std::vector<int> fnws = M.over_threads ? nws : std::vector<int>{8, 4};
+        std::vector<int> ftps = M.over_tp ? tps : std::vector<int>{16, 8, 4, 2};
+        for (int nw : fnws)
+            for (size_t i = 0; i < ftps.size(); ++i) {
+                const int tp = ftps[i];
+                const size_t sm = pjb::fastd_smem(c->n, c->m, c->k, c->d, nw, tp);
+                if (sm > c->smem_optin) continue;
+                consider(2, nw, tp, sm, pjb::fastd_blocks_per_sm(c->k, c->d, nw * 32, sm), int(ftps.size() - i));
+            }
+    }
     if (best_score < 0) {
         for (int nw : nws)
             for (int tp : tps) {
@@ -621,10 +633,12 @@ int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, d
     cudaGetDevice(&prev);
     if (prev != ctx->device) PJ_CUDA(cudaSetDevice(ctx->device));
     const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
-    cudaError_t e = L.variant > 0 ? pjb::launch_fast(ctx->k, L, ctx->dev(pi), d_points, d_out, (long long)batch,
-                                                    (cudaStream_t)stream)
-                                   : pjb::launch_eval(pi + 1, order_of(flags), L, ctx->dev(pi), d_points, d_out,
-                                                      (long long)batch, (cudaStream_t)stream);
+    cudaError_t e = L.variant == 1 ? pjb::launch_fast(ctx->k, L, ctx->dev(pi), d_points, d_out, (long long)batch,
+                                                     (cudaStream_t)stream)
+                    : L.variant == 2 ? pjb::launch_fastd(ctx->k, L, ctx->dev(pi), d_points, d_out, (long long)batch,
+                                                         (cudaStream_t)stream)
+                                     : pjb::launch_eval(pi + 1, order_of(flags), L, ctx->dev(pi), d_points, d_out,
+                                                        (long long)batch, (cudaStream_t)stream);
     if (prev != ctx->device) cudaSetDevice(prev);
     if (e) return cuda_fail(e, "evaluate: kernel launch");
     g_err.clear();
@@ -894,14 +908,18 @@ int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points) {
 int pj_set_kernel_variant(pj_ctx* ctx, int flags, int variant) {
     if (!ctx) return fail(PJ_EINVAL, "null context");
     if (ctx->host_only) return fail(PJ_EINVAL, "host-only context");
-    if (mode_of(flags) != kModeDDFast) return fail(PJ_EINVAL, "kernel variants exist for the fast dd order only");
+    const int md = mode_of(flags);
+    if (md == kModeDDRef) return fail(PJ_EINVAL, "kernel variants exist for complex double and the fast dd order");
     if (variant > 1 || variant < -1) return fail(PJ_EINVAL, "unknown kernel variant");
-    if (variant == 1 && !pjb::fast_supported(ctx->k)) return fail(PJ_EINVAL, "no specialised kernel for this k");
-    ctx->mode[kModeDDFast].over_variant = variant;
+    if (variant == 1 && md == kModeDDFast && !pjb::fast_supported(ctx->k))
+        return fail(PJ_EINVAL, "no specialised kernel for this k");
+    if (variant == 1 && md == kModeD && !pjb::fastd_supported(ctx->k))
+        return fail(PJ_EINVAL, "no specialised kernel for this k");
+    ctx->mode[md].over_variant = variant;
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(ctx->device);
-    int rc = choose_launch(ctx, kModeDDFast);
+    int rc = choose_launch(ctx, md);
     cudaSetDevice(prev);
     if (!rc) g_err.clear();
     return rc;

@@ -46,7 +46,8 @@ constexpr uint32_t kSchFlush = 1u << 23;
 constexpr uint32_t kSchValid = 1u << 24;
 
 struct LaunchCfg {
-    int variant = -1;         // 1 = fast kernel (eval_fast.cu), -1 = generic kernel
+    int variant = -1;         // 1 = fast dd kernel (eval_fast.cu), 2 = fast d kernel (eval_fastd.cu),
+                              // -1 = generic kernel
     int blocks = 0;
     int threads = 256;
     int tp = 1;               // points per CTA tile
@@ -66,6 +67,13 @@ int fast_plane_stride(int n);
 cudaError_t launch_fast(int k, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
                         cudaStream_t st);
 int fast_blocks_per_sm(int k, int n, int d, int threads, size_t smem);
+
+// fast complex-double kernels in the reference order (eval_fastd.cu), k in [1, 16], byte encoding
+bool fastd_supported(int k);
+size_t fastd_smem(int n, int m, int k, int d, int nw, int tp);
+cudaError_t launch_fastd(int k, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
+                         cudaStream_t st);
+int fastd_blocks_per_sm(int k, int d, int threads, size_t smem);
 
 // Newton corrector (newton.cu): per point, solve J dx = y - f from the
 // evaluator's output and write x + dx
