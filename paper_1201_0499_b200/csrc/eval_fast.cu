@@ -39,14 +39,15 @@ __device__ __forceinline__ CDD shfl_cdd(const CDD& v, int src) {
 __device__ __forceinline__ CDD sel_cdd(bool c, const CDD& a, const CDD& b) {
     return {c ? a.rh : b.rh, c ? a.rl : b.rl, c ? a.ih : b.ih, c ? a.il : b.il};
 }
-__device__ __forceinline__ CDD ld_pl(const double* p, int stride) {
-    return {p[0], p[stride], p[2 * stride], p[3 * stride]};
+// "hi/lo pair" layout: element e of an array keeps (re_hi, im_hi) at base + 2e and (re_lo, im_lo)
+// at base + hl + 2e — one 16-byte access per pair (LDS.128), half the instructions of four planes
+__device__ __forceinline__ CDD ld_hl(const double* p, int hl) {
+    const double2 h = *reinterpret_cast<const double2*>(p), l = *reinterpret_cast<const double2*>(p + hl);
+    return {h.x, l.x, h.y, l.y};
 }
-__device__ __forceinline__ void st_pl(double* p, int stride, const CDD& v) {
-    p[0] = v.rh;
-    p[stride] = v.rl;
-    p[2 * stride] = v.ih;
-    p[3 * stride] = v.il;
+__device__ __forceinline__ void st_hl(double* p, int hl, const CDD& v) {
+    *reinterpret_cast<double2*>(p) = make_double2(v.rh, v.ih);
+    *reinterpret_cast<double2*>(p + hl) = make_double2(v.rl, v.il);
 }
 __device__ __forceinline__ CDD ldg_coef(const double* q, int nm) {
     return {__ldg(q), __ldg(q + nm), __ldg(q + 2 * nm), __ldg(q + 3 * nm)};
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
     constexpr int W = 4;
     constexpr int R = K + 1;                 // stage-3 schedule entries per lane
     constexpr int stgW = (K + 1) * W * 32;   // staging doubles per warp
-    extern __shared__ double smem_[];
+    extern __shared__ __align__(16) double smem_[];
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = S.n, m = S.m, d = S.d, C = S.chunks;
     const int D1 = d > 2 ? d - 1 : 1;
@@ -111,18 +112,18 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
             const int t = i / n, v = i - t * n;
             CDD x = ld_aos(pts + ((b0 + t) * n + v) * W);
             if (!fin(x)) atomicOr(flag, 1);
-            st_pl(tab + t * tabPt + v, NS, x);
+            st_hl(tab + t * tabPt + 2 * v, 2 * NS, x);
         }
         __syncthreads();
         if (!D2) {  // power chains, ref kernels.cpp:16-24 (normalised products: shared table)
             for (int i = threadIdx.x; i < tp * n; i += blockDim.x) {
                 const int t = i / n, v = i - t * n;
-                double* pb = tab + t * tabPt + v;
-                const CDD x = ld_pl(pb, NS);
+                double* pb = tab + t * tabPt + 2 * v;
+                const CDD x = ld_hl(pb, 2 * NS);
                 CDD r = x;
                 for (int e = 2; e < d; ++e) {
                     r = cdd_mul(r, x);
-                    st_pl(pb + (e - 1) * W * NS, NS, r);
+                    st_hl(pb + (e - 1) * W * NS, 2 * NS, r);
                 }
             }
             __syncthreads();
@@ -176,7 +177,7 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
                                 __fma_rn(x.il, a, __fma_rn(x.ih, a, -pi))};
                     }
                 };
-                auto X = [&](int j) -> CDD { return ld_pl(xt + POS(j), NS); };
+                auto X = [&](int j) -> CDD { return ld_hl(xt + 2 * POS(j), 2 * NS); };
                 // x^(a_j - 1): branch-free. d <= 2 (D2): select between 1 and the gathered x;
                 // otherwise a table load (row max(a_j - 2, 0)) and a select for a_j == 1
                 auto PWsel = [&](int j, const CDD& v) -> CDD {
@@ -185,10 +186,10 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
                     } else {
                         const int e1 = EX1(j);
                         const int e = e1 > 0 ? e1 - 1 : 0;
-                        return sel_cdd(e1 != 0, ld_pl(xt + e * W * NS + POS(j), NS), one);
+                        return sel_cdd(e1 != 0, ld_hl(xt + e * W * NS + 2 * POS(j), 2 * NS), one);
                     }
                 };
-                auto SLOT = [&](int j) -> double* { return stg + j * W * 32 + lane; };
+                auto SLOT = [&](int j) -> double* { return stg + j * W * 32 + 2 * lane; };
 
                 // ---- stage 1 + forward products (interleaved chains); chain states are
                 // compile-time after unrolling: F_j is normalised iff j is odd, f_j iff j is even;
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
                     const CDD v0 = X(0);
                     f = PWsel(0, v0);
                     Fc = v0;
-                    st_pl(SLOT(1), 32, v0);
+                    st_hl(SLOT(1), 64, v0);
                 }
 #pragma unroll
                 for (int j = 1; j < K; ++j) {
@@ -206,7 +207,7 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
                     f = cmul_n((j & 1) == 0, f, PWsel(j, v));
                     if (j < K - 1) {
                         Fc = cmul_n((j & 1) == 0, Fc, v);
-                        if (j + 1 < K - 1) st_pl(SLOT(j + 1), 32, Fc);
+                        if (j + 1 < K - 1) st_hl(SLOT(j + 1), 64, Fc);
                     } else {
                         vlast = v;
                     }
@@ -221,18 +222,18 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
                     const CDD cval = {__ldg(cf), __ldg(cf + 32), __ldg(cf + 64), __ldg(cf + 96)};
                     const CDD q0 = cmul_n(!f_norm, f, cval);  // normalised iff f was not
                     const CDD L = cdd_mul_u(Fc, q0);
-                    st_pl(SLOT(K - 1), 32, SCALE(K - 1, L));
-                    st_pl(SLOT(K), 32, cdd_mul(L, vlast));
+                    st_hl(SLOT(K - 1), 64, SCALE(K - 1, L));
+                    st_hl(SLOT(K), 64, cdd_mul(L, vlast));
                     q = cmul_n(f_norm, q0, vlast);
                 }
 #pragma unroll
                 for (int j = K - 2; j >= 1; --j) {
                     const bool q_norm = (((K - 2 - j) & 1) == 0) ? f_norm : !f_norm;  // state of q here
-                    const CDD L = cdd_mul_u(ld_pl(SLOT(j), 32), q);
-                    st_pl(SLOT(j), 32, SCALE(j, L));
+                    const CDD L = cdd_mul_u(ld_hl(SLOT(j), 64), q);
+                    st_hl(SLOT(j), 64, SCALE(j, L));
                     q = cmul_n(!q_norm, q, X(j));
                 }
-                st_pl(SLOT(0), 32, SCALE(0, q));
+                st_hl(SLOT(0), 64, SCALE(0, q));
                 __syncwarp();
 #ifdef PJB_EXP_NO_STAGE3
                 if (codes[0] != 0xdeadbeefu) continue;  // experiment: stage 2 only
@@ -251,8 +252,8 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
                         const uint32_t code = codes[r];
                         if (code & kSchValid) {
                             const int ent = code & 0x1fff;
-                            double* sl = stg + (ent >> 5) * W * 32 + (ent & 31);
-                            const CDD tv = ld_pl(sl, 32);
+                            double* sl = stg + (ent >> 5) * W * 32 + 2 * (ent & 31);
+                            const CDD tv = ld_hl(sl, 64);
                             const DD a = two_sum(sr, tv.rh), b = two_sum(si, tv.ih);
                             sr = a.hi;
                             si = b.hi;
@@ -261,7 +262,7 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
                             if (code & kSchFlush) {
                                 // the partial overwrites the staging slot this lane just consumed
                                 // (each slot is read exactly once, by this lane): no extra smem
-                                st_pl(sl, 32, CDD{sr, lr, si, li});
+                                st_hl(sl, 64, CDD{sr, lr, si, li});
                                 sr = lr = si = li = 0.0;
                             }
                         }
@@ -277,18 +278,18 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
                     if (o > n) continue;
                     const uint32_t sd = k2 == 0 ? sd0 : __ldg(S.seg + pc * (n + 1) + o);
                     const int first = sd & 0xffff, cnt = sd >> 16;
-                    CDD r = c == 0 ? zero : ld_pl(acc + o, n + 1);
+                    CDD r = c == 0 ? zero : ld_hl(acc + 2 * o, 2 * (n + 1));
                     const uint16_t* sgc = S.segcode + pc * S.nseg + first;
                     int qq = 0;
                     if (cnt > 0) {
                         const int e = k2 == 0 ? seg0 : __ldg(sgc);
-                        const CDD sv = ld_pl(stg + (e >> 5) * W * 32 + (e & 31), 32);
+                        const CDD sv = ld_hl(stg + (e >> 5) * W * 32 + 2 * (e & 31), 64);
                         r = c == 0 ? sv : cdd_add(r, sv);
                         qq = 1;
                     }
                     for (; qq < cnt; ++qq) {
                         const int e = __ldg(sgc + qq);
-                        r = cdd_add(r, ld_pl(stg + (e >> 5) * W * 32 + (e & 31), 32));
+                        r = cdd_add(r, ld_hl(stg + (e >> 5) * W * 32 + 2 * (e & 31), 64));
                     }
                     if (last) {
                         if (t < tp) {
@@ -296,7 +297,7 @@ __global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSyst
                             st_aos(out + ((b0 + t) * nout + at) * W, cdd_renorm(r));
                         }
                     } else {
-                        st_pl(acc + o, n + 1, r);
+                        st_hl(acc + 2 * o, 2 * (n + 1), r);
                     }
                 }
                 __syncwarp();
