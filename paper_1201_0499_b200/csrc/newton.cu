@@ -30,9 +30,9 @@
 // augmented matrix [J | rhs] lives in shared memory as W planes of n × (n+1) doubles (row
 // stride n+1); n ≤ 64 fits (133 KB in dd), larger systems use a per-CTA global slab with the
 // same code. Warp 0 runs one column ahead ("look-ahead"): during step kk it updates column
-// kk+1 of the active rows (the values stay in its registers), picks piv_{kk+1} by a shuffle
-// arg-max, forms the pivot inverse and the multipliers of column kk+1 and the next active-row
-// list — while warps 1.. update columns kk+2..n of step kk (a thread keeps one pivot-row element
+// kk+1 of the active rows (the values stay in its registers), picks piv_{kk+1} by a redux
+// arg-max while every lane inverts its own candidates speculatively, broadcasts the winner's
+// inverse and forms the multipliers of column kk+1 and the next active-row list — while warps 1.. update columns kk+2..n of step kk (a thread keeps one pivot-row element
 // in registers and walks rows). One barrier per step. Back substitution runs in warp 0 with the
 // right-hand side in registers (a lane owns rows lane + 32q) and each solved component
 // broadcast by shuffle. Several CTAs per SM overlap one CTA's serial phases with the others'
@@ -140,6 +140,10 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
     // Warp-0 look-ahead for column c: rows list[0..R) (values v[] already in registers), pick the
     // pivot, store inv_c and the multipliers of column c, write the next list (R-1 rows).
     auto pivot_phase = [&](int c, const int* list, int R, const T* v, int* next) {
+        // every lane inverts its own candidates speculatively, off the arg-max's critical path
+        T ivq[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) ivq[q] = nt_inv(v[q]);
         double best = 0.0;
         int bi = -1, bq = 0;
 #pragma unroll
@@ -155,27 +159,26 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
                 }
             }
         }
-        for (int o = 16; o; o >>= 1) {
-            const double ob = __shfl_xor_sync(0xffffffffu, best, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
-            if (ob > best || (ob == best && oi >= 0 && (bi < 0 || oi < bi))) {
-                best = ob;
-                bi = oi;
-                bq = oq;
-            }
-        }
-        if (bi < 0) {
+        // arg-max over the warp with redux: the largest magnitude (its bits are monotonic, high
+        // word then low word), ties to the smallest row — the same rule as a sequential scan
+        const unsigned long long bits = __double_as_longlong(best);
+        const unsigned hi = unsigned(bits >> 32), lo = unsigned(bits);
+        const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+        const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+        const bool cand = bi >= 0 && hi == mh && lo == ml;
+        const int rmin = __reduce_min_sync(0xffffffffu, cand ? bi : 0x7fffffff);
+        if (rmin == 0x7fffffff) {
             if (lane == 0) s_sing = 1;
             return;
         }
-        // broadcast the pivot value from its owner, every lane forms the same inverse
-        T pv = v[0];
+        const int owner = __ffs(__ballot_sync(0xffffffffu, cand && bi == rmin)) - 1;
+        bi = rmin;
+        bq = __shfl_sync(0xffffffffu, bq, owner);
+        T iv = ivq[0];
 #pragma unroll
         for (int q = 1; q < NQ; ++q)
-            if (q == (bq >> 5)) pv = v[q];
-        pv = shfl_idx(pv, bq & 31);
-        const T iv = nt_inv(pv);
+            if (q == (bq >> 5)) iv = ivq[q];
+        iv = shfl_idx(iv, owner);
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
             const int idx = lane + 32 * q;
