@@ -197,10 +197,21 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
     };
     for (long long b = blockIdx.x; b < a.B; b += gridDim.x) {
         const double* ev = a.evals + size_t(b) * nout * W;
-        // ---- load [J | y − f] into planes
-        for (int t = tid; t < n * n; t += nt) {
-            const int i = t / n, j = t - i * n;
-            S::st_planes(A + i * ld + j, P, S::ld_aos(ev + size_t(n + t) * W));
+        // ---- load [J | y − f] into planes. Shared-memory matrices: 8-byte cp.async copies straight
+        // into the planes (no registers, every copy in flight at once); global slabs: plain loads
+        if (!a.gscratch) {
+            for (int t = tid; t < n * n * W; t += nt) {
+                const int el = t / W, comp = t - el * W;
+                const int i = el / n, j = el - i * n;
+                const unsigned dst = unsigned(__cvta_generic_to_shared(A + size_t(comp) * P + i * ld + j));
+                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(ev + size_t(n) * W + t));
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+        } else {
+            for (int t = tid; t < n * n; t += nt) {
+                const int i = t / n, j = t - i * n;
+                S::st_planes(A + i * ld + j, P, S::ld_aos(ev + size_t(n + t) * W));
+            }
         }
         if (warp == 0) {
             double rn = 0.0;
@@ -217,6 +228,7 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
                 s_sing = 0;
             }
         }
+        asm volatile("cp.async.wait_all;\n" ::);
         __syncthreads();
         // ---- column 0: pivot, inverse, multipliers
         if (warp == 0) {
