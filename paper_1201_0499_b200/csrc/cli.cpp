@@ -4,7 +4,10 @@
 //
 //   polyjac_b200 generate --n N --m M --k K --d D [--seed S] --out PATH
 //   polyjac_b200 bench (--system PATH | --n N --m M --k K --d D) [--seed S] [--evals E]
-//                      [--points B] [--precision dd|d] [--device G]
+//                      [--points B] [--precision dd|d] [--device G] [--gpus G]
+//     --gpus G shards the E evaluations over devices 0..G-1 (one context and host thread per
+//     device, contiguous shards of one point stream, system replicated, no collective) and
+//     reports the aggregate rate over the slowest device
 //   polyjac_b200 check --system PATH [--points P] [--seed S] [--tol T] [--device G]
 //
 // The correctness gate compares the two device arithmetic paths with each other: the complex
@@ -23,6 +26,7 @@
 #include <cstring>
 #include <map>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/polyjac_b200.h"
@@ -81,7 +85,7 @@ void usage(FILE* f) {
                  "  generate --n N --m M --k K --d D [--seed S] --out PATH\n"
                  "      write a random benchmark system file\n"
                  "  bench (--system PATH | --n N --m M --k K --d D) [--seed S] [--evals E] [--points B]\n"
-                 "        [--precision dd|d] [--device G]\n"
+                 "        [--precision dd|d] [--device G] [--gpus G]\n"
                  "      timed evaluation with a correctness gate; prints a RESULT key=value line\n"
                  "  check --system PATH [--points P] [--seed S] [--tol T] [--device G]\n"
                  "      complex double vs complex double-double on random points\n");
@@ -211,6 +215,15 @@ int cmd_bench(const Args& a) {
     if (a.kv.count("points") && (!get_int(a, "points", &points) || points < 1))
         return usage_error("--points must be >= 1");
     if (a.kv.count("device") && !get_int(a, "device", &device)) return usage_error("bad --device");
+    int64_t gpus = 1;
+    if (a.kv.count("gpus") && (!get_int(a, "gpus", &gpus) || gpus < 1)) return usage_error("--gpus must be >= 1");
+    if (gpus > 1) {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess) ndev = 0;
+        if (gpus > ndev) return usage_error("--gpus " + std::to_string(gpus) + " exceeds the " + std::to_string(ndev) +
+                                            " visible device(s)");
+        device = 0;
+    }
     std::string prec = a.kv.count("precision") ? a.kv.at("precision") : "dd";
     if (prec != "dd" && prec != "d") return usage_error("--precision must be dd or d");
     Sys S;
@@ -237,44 +250,93 @@ int cmd_bench(const Args& a) {
         pj_ctx_destroy(ctx);
         return 1;
     }
-    // device-resident timing of `evals` evaluations in batches of B points, each precision
+    // device-resident timing of `evals` evaluations in batches of B points, each precision; with
+    // --gpus G the evaluations are sharded over devices 0..G-1, one host thread and context each
     const size_t nout = size_t(n) * n + n;
-    auto time_prec = [&](int flags, int W, double* ms) -> int {
+    auto time_prec = [&](pj_ctx* c, int dev, int64_t first, int64_t count, int flags, int W, double* ms) -> int {
         double *dp = nullptr, *dout = nullptr;
-        std::vector<double> host(size_t(B) * n * W, 0.0);
-        for (size_t i = 0; i < size_t(B) * n; ++i) {
-            host[W * i] = pts[2 * i];
-            host[W * i + (W == 4 ? 2 : 1)] = pts[2 * i + 1];
+        const int64_t Bd = std::min(B, count);
+        std::vector<double> p2(size_t(Bd) * n * 2), host(size_t(Bd) * n * W, 0.0);
+        pj_random_points_range(n, first, Bd, uint64_t(seed) ^ kPointSeedSalt, p2.data());
+        for (size_t i = 0; i < size_t(Bd) * n; ++i) {
+            host[W * i] = p2[2 * i];
+            host[W * i + (W == 4 ? 2 : 1)] = p2[2 * i + 1];
         }
-        if (cudaSetDevice(int(device)) || cudaMalloc(&dp, host.size() * 8) || cudaMalloc(&dout, size_t(B) * nout * W * 8) ||
+        if (cudaSetDevice(dev) || cudaMalloc(&dp, host.size() * 8) || cudaMalloc(&dout, size_t(Bd) * nout * W * 8) ||
             cudaMemcpy(dp, host.data(), host.size() * 8, cudaMemcpyHostToDevice))
             return PJ_ECUDA;
-        int rc = pj_evaluate(ctx, flags, dp, B, dout, nullptr);  // warm-up
+        cudaStream_t st;
+        cudaStreamCreate(&st);
+        int rc = pj_evaluate(c, flags, dp, Bd, dout, st);  // warm-up
         cudaEvent_t e0, e1;
         cudaEventCreate(&e0);
         cudaEventCreate(&e1);
-        cudaEventRecord(e0);
-        for (int64_t done = 0; done < evals && rc == PJ_OK; done += B)
-            rc = pj_evaluate(ctx, flags, dp, std::min(B, evals - done), dout, nullptr);
-        cudaEventRecord(e1);
+        cudaEventRecord(e0, st);
+        for (int64_t done = 0; done < count && rc == PJ_OK; done += Bd)
+            rc = pj_evaluate(c, flags, dp, std::min(Bd, count - done), dout, st);
+        cudaEventRecord(e1, st);
         cudaEventSynchronize(e1);
         float f = 0;
         cudaEventElapsedTime(&f, e0, e1);
         *ms = f;
         cudaEventDestroy(e0);
         cudaEventDestroy(e1);
+        cudaStreamDestroy(st);
         cudaFree(dp);
         cudaFree(dout);
         return rc;
     };
+    struct DevRun {
+        int dev = 0;
+        pj_ctx* ctx = nullptr;
+        int64_t first = 0, count = 0;
+        double ms_d = 0, ms_dd = 0;
+        int rc = PJ_OK;
+        std::string err;
+    };
+    std::vector<DevRun> runs(static_cast<size_t>(gpus));
+    for (int g = 0; g < gpus; ++g) {
+        DevRun& r = runs[g];
+        r.dev = gpus > 1 ? g : int(device);
+        r.first = evals * g / gpus;
+        r.count = evals * (g + 1) / gpus - r.first;
+        r.ctx = g == 0 && r.dev == int(device) ? ctx : nullptr;
+    }
+    auto worker = [&](DevRun& r) {
+        if (!r.ctx && pj_ctx_create(&S.desc, r.dev, &r.ctx) != PJ_OK) {
+            r.rc = PJ_ECUDA;
+            r.err = pj_last_error();
+            return;
+        }
+        if (r.count == 0) return;
+        r.rc = time_prec(r.ctx, r.dev, r.first, r.count, PJ_PREC_D, 2, &r.ms_d);
+        if (r.rc == PJ_OK && prec == "dd") r.rc = time_prec(r.ctx, r.dev, r.first, r.count, PJ_PREC_DD, 4, &r.ms_dd);
+        if (r.rc != PJ_OK) r.err = pj_last_error();
+    };
+    std::vector<std::thread> th;
+    for (auto& r : runs) th.emplace_back(worker, std::ref(r));
+    for (auto& t : th) t.join();
     double ms_d = 0, ms_dd = 0;
-    int rc = time_prec(PJ_PREC_D, 2, &ms_d);
-    if (rc == PJ_OK && prec == "dd") rc = time_prec(PJ_PREC_DD, 4, &ms_dd);
+    int rc = PJ_OK;
+    for (auto& r : runs) {
+        if (r.rc != PJ_OK && rc == PJ_OK) {
+            rc = r.rc;
+            std::fprintf(stderr, "error (device %d): %s\n", r.dev, r.err.c_str());
+        }
+        ms_d = std::max(ms_d, r.ms_d);  // the job ends with its slowest device
+        ms_dd = std::max(ms_dd, r.ms_dd);
+    }
+    for (auto& r : runs)
+        if (r.ctx && r.ctx != ctx) pj_ctx_destroy(r.ctx);
     if (rc != PJ_OK) {
-        std::fprintf(stderr, "error: %s\n", pj_last_error());
         pj_ctx_destroy(ctx);
         return 2;
     }
+    if (gpus > 1)
+        for (auto& r : runs)
+            std::printf("device %d: evaluations [%lld, %lld): complex double %.3f ms, %s %.3f ms\n", r.dev,
+                        (long long)r.first, (long long)(r.first + r.count), r.ms_d, prec.c_str(),
+                        prec == "dd" ? r.ms_dd : r.ms_d);
     const double ms = prec == "dd" ? ms_dd : ms_d;
     uint64_t cnt[5];
     pj_mult_counts(ctx, evals, cnt);
@@ -284,16 +346,16 @@ int cmd_bench(const Args& a) {
     const long long mults = (long long)(cnt[0] + cnt[1] + cnt[2] + cnt[4]);
     std::printf("system: n=%d m=%d k=%d d=%d (%lld monomials), footprint %lld bytes\n", S.desc.n, S.desc.m, S.desc.k,
                 S.desc.d, (long long)S.desc.n * S.desc.m, 2LL * S.desc.n * S.desc.m * S.desc.k);
-    std::printf("device %lld: %d-thread CTAs x %d, %lld evaluations in batches of %lld points\n", (long long)device,
-                threads, blocks, (long long)evals, (long long)B);
+    std::printf("device %lld: %d-thread CTAs x %d, %lld evaluations in batches of %lld points over %lld GPU(s)\n",
+                (long long)device, threads, blocks, (long long)evals, (long long)B, (long long)gpus);
     std::printf("gate: %s\n", describe(gate, kGateTol, true).c_str());
     std::printf("complex double (reference order): %.3f ms; requested %s: %.3f ms (%.3e evals/s)\n", ms_d, prec.c_str(),
                 ms, evals / (ms * 1e-3));
     std::printf("RESULT n=%d m=%d k=%d d=%d monomials=%lld B=%d workers=1 evals=%lld baseline_ms=%.3f pipeline_ms=%.3f "
-                "speedup=%.3f mults=%lld footprint_bytes=%lld precision=%s points=%lld evals_per_s=%.6g gate_max_rel=%.3g\n",
+                "speedup=%.3f mults=%lld footprint_bytes=%lld precision=%s points=%lld evals_per_s=%.6g gate_max_rel=%.3g gpus=%lld\n",
                 S.desc.n, S.desc.m, S.desc.k, S.desc.d, (long long)S.desc.n * S.desc.m, threads, (long long)evals, ms_d,
                 ms, ms > 0 ? ms_d / ms : 0.0, mults, 2LL * S.desc.n * S.desc.m * S.desc.k, prec.c_str(), (long long)B,
-                evals / (ms * 1e-3), std::max(gate.max_value, gate.max_jac));
+                evals / (ms * 1e-3), std::max(gate.max_value, gate.max_jac), (long long)gpus);
     pj_ctx_destroy(ctx);
     return 0;
 }

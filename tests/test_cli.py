@@ -92,3 +92,19 @@ def test_bench_c2_shape(gpu):
     assert rc == 0, out
     kv = result_line(out)
     assert kv["precision"] == "dd" and float(kv["evals_per_s"]) > 1e6
+
+
+def test_gpus_beyond_visible_devices_is_a_usage_error():
+    rc, out = run("bench", "--n", 8, "--m", 4, "--k", 3, "--d", 2, "--gpus", 4096)
+    assert rc == 2 and "exceeds" in out
+    assert run("bench", "--n", 8, "--m", 4, "--k", 3, "--d", 2, "--gpus", 0)[0] == 2
+
+
+@pytest.mark.gpu
+def test_bench_multi_gpu_sharding(gpu):
+    import torch
+    g = torch.cuda.device_count()
+    rc, out = run("bench", "--n", 32, "--m", 32, "--k", 8, "--d", 2, "--seed", 7, "--evals", 65536, "--gpus", g)
+    assert rc == 0, out
+    kv = result_line(out)
+    assert kv["gpus"] == str(g) and float(kv["evals_per_s"]) > 1e6
