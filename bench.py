@@ -225,7 +225,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--order", default="fast", choices=["fast", "ref"])
     ap.add_argument("--no-extras", action="store_true",
-                    help="skip the secondary lines (C4 quality-up factor, f1 Newton step)")
+                    help="skip the secondary lines (C3, C4 quality-up factor, f1 Newton step)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     if args.impl == "reference":
@@ -402,6 +402,18 @@ def main():
                               "d_evals_per_s": B / (ms_d * 1e-3), "dd_evals_per_s": B / (kern_ms * 1e-3),
                               "dd_over_d_time": kern_ms / ms_d, "d_launch": ctx.launch("d")}
         del out_d
+        # C3: n=64 m=64 k=16 d=10 (higher degrees, larger common-factor stage), complex dd
+        s3 = pj.random_system(64, 64, 16, 10, SYS_SEED)
+        ctx3 = pj.EvaluationContext(s3, device=local)
+        B3 = 8192
+        p3 = torch.from_numpy(pj.to_dd(pj.random_points(64, B3, PT_SEED))).to(dev)
+        o3 = torch.empty((B3, 64 + 64 * 64, 4), dtype=torch.float64, device=dev)
+        ms3 = timed(lambda: ctx3.evaluate_device(p3, o3, "dd", args.order, stream), 5)
+        f3 = model_flops(64, 64, 16, 10)
+        line["c3"] = {"config": "C3: random_system(64,64,16,10,seed 7), 8,192 points, complex dd, fast order",
+                      "evals_per_s": B3 / (ms3 * 1e-3), "ms_per_batch": ms3, "flops_per_eval": f3,
+                      "roofline_frac": f3 * B3 / (ms3 * 1e-3) / 1e12 / peak, "launch": ctx3.launch("dd")}
+        del o3, p3, ctx3
         # f1: one Newton step (evaluate + solve) per point on device, complex dd
         xo = torch.empty_like(bufs[0])
         nst = torch.empty(B, dtype=torch.int32, device=dev)
