@@ -111,10 +111,13 @@ __device__ __forceinline__ CDD shfl_idx<CDD>(CDD v, int src) {
 // kRecip[c] = ceil(2^16 / c): floor(x / c) == (x * kRecip[c]) >> 16 for x, c <= 256
 __constant__ unsigned kRecip[257];
 
+#ifndef PJB_NT_MINB
+#define PJB_NT_MINB 6
+#endif
 // n <= 32 (NQ = 1) runs 128-thread CTAs, six per SM (the matrix is 36 KB in dd): 85 registers
 template <int NQ>
 struct NtBounds {
-    static constexpr int threads = NQ == 1 ? 128 : 256, blocks = NQ == 1 ? 6 : 1;
+    static constexpr int threads = NQ == 1 ? 128 : 256, blocks = NQ == 1 ? PJB_NT_MINB : 1;
 };
 template <class T, int NQ>
 __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) newton_kernel(NewtonArgs a) {
@@ -283,6 +286,34 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
                 // columns kk+2..n (Cp of them) for R rows: a thread keeps u = A[pr][j] in registers
                 // and walks rows rg, rg+G, ...
                 const int Cp = n - kk - 1, Tp = nt - 32, tp = tid - 32;
+                // measured (tools/nt_quick.py, C2/C3): column pairs win for complex double and
+                // n > 32 (n = 64 dd: 8.92 -> 8.40 ms), single columns for n <= 32 dd (7.80 vs 8.42 ms)
+                constexpr bool kPairs = NQ >= 2 || W == 2;
+                if constexpr (kPairs) {
+                // column pairs (j, j + Ch): one multiplier load serves two independent chains
+                const int Ch = (Cp + 1) >> 1;
+                for (int c0 = 0; c0 < Ch; c0 += Tp) {
+                    const int cw = min(Tp, Ch - c0);
+                    const unsigned rc = kRecip[cw];
+                    const int G = int((unsigned(Tp) * rc) >> 16), rg = int((unsigned(tp) * rc) >> 16);
+                    if (rg >= G) continue;
+                    const int ci = c0 + (tp - rg * cw);
+                    const int j1 = kk + 2 + ci, j2 = j1 + Ch;
+                    const bool two = ci + Ch < Cp;
+                    const T u1 = S::ld_planes(A + pr * ld + j1, P);
+                    const T u2 = two ? S::ld_planes(A + pr * ld + j2, P) : u1;
+                    for (int idx = rg; idx < R; idx += G) {
+                        const int r = list[idx];
+                        const T l = S::ld_planes(A + r * ld + kk, P);
+                        const T v1 = S::ld_planes(A + r * ld + j1, P);
+                        const T v2 = two ? S::ld_planes(A + r * ld + j2, P) : v1;
+                        const T w1 = S::add(v1, nt_neg(nt_umul(l, u1)));
+                        const T w2 = S::add(v2, nt_neg(nt_umul(l, u2)));
+                        S::st_planes(A + r * ld + j1, P, w1);
+                        if (two) S::st_planes(A + r * ld + j2, P, w2);
+                    }
+                }
+                } else {
                 for (int c0 = 0; c0 < Cp; c0 += Tp) {
                     const int cw = min(Tp, Cp - c0);
                     const unsigned rc = kRecip[cw];
@@ -290,14 +321,13 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
                     if (rg >= G) continue;
                     const int j = kk + 2 + c0 + (tp - rg * cw);
                     const T u = S::ld_planes(A + pr * ld + j, P);
-                    // (a software-pipelined walk — next row's loads before this row's store — measured
-                    // 5% slower at n = 32 dd, 8% faster at n = 64: kept simple)
                     for (int idx = rg; idx < R; idx += G) {
                         const int r = list[idx];
                         const T l = S::ld_planes(A + r * ld + kk, P);
                         const T v = S::ld_planes(A + r * ld + j, P);
                         S::st_planes(A + r * ld + j, P, S::add(v, nt_neg(nt_umul(l, u))));
                     }
+                }
                 }
             }
             __syncthreads();
