@@ -270,7 +270,9 @@ int choose_launch(pj_ctx* c, int mode) {
         // measured (tools/tune.py): 8-warp CTAs beat more, smaller CTAs at equal residency;
         // at equal residency 2-point tiles are best (C1: 0.853 vs 0.851 (1); C3: 0.763 vs 0.72 (4))
         std::vector<int> ftps = M.over_tp ? tps : std::vector<int>{2, 4, 1};
-        std::vector<int> fnws = M.over_threads ? nws : std::vector<int>{8};
+        // k > 12: per-warp staging (k+1 slots x 32 lanes x 32 B) caps residency; wider CTAs with
+        // one-point tiles fit more warps per SM (C3: 10 warps vs 8)
+        std::vector<int> fnws = M.over_threads ? nws : (c->k > 12 ? std::vector<int>{8, 10, 12} : std::vector<int>{8});
         for (int nw : fnws)
             for (size_t i = 0; i < ftps.size(); ++i) {
                 const int tp = ftps[i];
@@ -884,7 +886,8 @@ int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points) {
     if (ctx->host_only) return fail(PJ_EINVAL, "host-only context");
     const int pi = prec_index(flags);
     if (pi < 0) return fail(PJ_EINVAL, "unknown precision flag");
-    if (threads < 0 || threads > 256 || threads % 32) return fail(PJ_EINVAL, "threads must be a multiple of 32 <= 256");
+    if (threads < 0 || threads > 384 || threads % 32)
+        return fail(PJ_EINVAL, "threads must be a multiple of 32 <= 384 (<= 256 except the fast dd kernel for k > 12)");
     if (tile_points < 0) return fail(PJ_EINVAL, "tile_points must be >= 0");
     if (flags & PJ_OP_NEWTON) {
         if (threads == 32) return fail(PJ_EINVAL, "newton: threads must be >= 64");

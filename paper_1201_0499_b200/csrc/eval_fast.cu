@@ -81,11 +81,15 @@ __device__ __forceinline__ bool fin(const CDD& v) {
 // Register budget: 3 CTAs x 256 threads (<= 85 registers) for k <= 12, where the per-warp
 // staging also fits three CTAs; 2 CTAs (<= 128 registers) above. Measured with tools/tune.py:
 // k = 8: 0.853 (3 CTAs) vs 0.843 (2 CTAs); k = 16: 0.763 (2 CTAs) vs 0.723 (3 CTAs).
+// k > 12: CTAs of up to 16 warps (one per SM when the staging of 8+ warps fills shared memory);
+// (512, 1) keeps the 128-register budget of (256, 2).
 template <int K>
-constexpr int fast_min_blocks() { return K <= 12 ? 3 : 2; }
+constexpr int fast_min_blocks() { return K <= 12 ? 3 : 1; }
+template <int K>
+constexpr int fast_max_threads() { return K <= 12 ? 256 : 512; }
 
 template <int K, int NS, bool D2>
-__global__ void __launch_bounds__(256, fast_min_blocks<K>()) fast_kernel(DevSystem S, const double* __restrict__ pts,
+__global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) fast_kernel(DevSystem S, const double* __restrict__ pts,
                                                    double* __restrict__ out, long long B, int TP,
                                                    int* __restrict__ flag) {
     constexpr int W = 4;

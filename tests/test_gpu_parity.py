@@ -296,6 +296,22 @@ def test_fast_kernel_launch_shape_invariance(gpu):
             assert np.array_equal(ctx.evaluate_dd(p4).view(np.uint64), base.view(np.uint64))
 
 
+def test_fast_kernel_wide_ctas_for_large_k(gpu):
+    # k > 12: CTAs of up to 16 warps (one SM-filling CTA when the staging dominates shared memory)
+    s = pj.random_system(24, 20, 16, 3, 77)
+    S = sysd_of(s)
+    ctx = pj.EvaluationContext(s)
+    p4 = stress_dd(pj.random_points(24, 41, 78), 5)
+    want, ms = O.evaluate("dd", S, p4, magsum=True)
+    base = ctx.evaluate_dd(p4)
+    assert dd_rel(base, want, ms) <= DD_TOL
+    for threads in (256, 320, 384):  # 16 warps of staging would exceed shared memory at k = 16
+        for tp in (1, 2):
+            ctx.set_launch("dd", threads, tp)
+            assert ctx.launch("dd")["variant"] == 1
+            assert np.array_equal(ctx.evaluate_dd(p4).view(np.uint64), base.view(np.uint64))
+
+
 def test_dd_contract_under_cancellation(gpu):
     """Adversarial inputs: duplicated monomials with opposite coefficients (exact cancellation
     in every stage-3 sum), unit-modulus points (no decay along k = 16 product chains, d = 10),
