@@ -270,9 +270,9 @@ int choose_launch(pj_ctx* c, int mode) {
         // measured (tools/tune.py): 8-warp CTAs beat more, smaller CTAs at equal residency;
         // at equal residency 2-point tiles are best (C1: 0.853 vs 0.851 (1); C3: 0.763 vs 0.72 (4))
         std::vector<int> ftps = M.over_tp ? tps : std::vector<int>{2, 4, 1};
-        // k > 12: per-warp staging (k+1 slots x 32 lanes x 32 B) caps residency; wider CTAs with
-        // one-point tiles fit more warps per SM (C3: 10 warps vs 8)
-        std::vector<int> fnws = M.over_threads ? nws : (c->k > 12 ? std::vector<int>{8, 10, 12} : std::vector<int>{8});
+        // (k > 12 admits 10-16 warp CTAs via pj_set_launch; measured at C3: 10 warps, 18.0 ms vs
+        // 8 warps, 17.1 ms — the automatic choice stays at 8)
+        std::vector<int> fnws = M.over_threads ? nws : std::vector<int>{8};
         for (int nw : fnws)
             for (size_t i = 0; i < ftps.size(); ++i) {
                 const int tp = ftps[i];
