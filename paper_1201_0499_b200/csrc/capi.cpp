@@ -128,6 +128,8 @@ struct pj_ctx {
     uint16_t* d_gm_ent = nullptr;
     std::vector<uint32_t> sch, seg;  // fast-kernel stage-3 schedule (host copies)
     std::vector<uint16_t> segcode;
+    std::vector<uint32_t> segq;  // [(p*C + c)*(n+1) + o] x 4 words, see pj_ctx_create
+    uint32_t* d_segq = nullptr;
     uint32_t* d_sch = nullptr;
     uint32_t* d_seg = nullptr;
     uint16_t* d_segcode = nullptr;
@@ -177,6 +179,7 @@ struct pj_ctx {
         S.seg = d_seg;
         S.nseg = nseg;
         S.segcode = d_segcode;
+        S.segq = reinterpret_cast<const uint4*>(d_segq);
         S.coefT = d_coefT;
         return S;
     }
@@ -200,6 +203,7 @@ void free_ctx(pj_ctx* c) {
     cudaFree(c->d_sch);
     cudaFree(c->d_seg);
     cudaFree(c->d_segcode);
+    cudaFree(c->d_segq);
     cudaFree(c->d_flag);
     cudaFree(c->d_coef[0]);
     cudaFree(c->d_coef[1]);
@@ -537,6 +541,18 @@ int pj_ctx_create_ex(const pj_system_desc* sys, int device, int options, pj_ctx*
                     }
                 }
             }
+        // per-output 16-byte record for phase 2: first | count << 16 and the first six segment codes
+        // inline (one load per output instead of a dependent code load per segment)
+        c->segq.assign(size_t(n) * C * (n + 1) * 4, 0);
+        for (size_t pc = 0; pc < size_t(n) * C; ++pc)
+            for (int o = 0; o <= n; ++o) {
+                const uint32_t sd = c->seg[pc * (n + 1) + o];
+                const int first = sd & 0xffff, cnt = sd >> 16;
+                uint32_t* q = c->segq.data() + (pc * (n + 1) + o) * 4;
+                q[0] = sd;
+                for (int i = 0; i < std::min(cnt, 6); ++i)
+                    q[1 + i / 2] |= uint32_t(c->segcode[pc * c->nseg + first + i]) << (16 * (i & 1));
+            }
     }
 
     if (device < 0) {  // host-only context: packing and index maps, no device residency
@@ -569,6 +585,7 @@ int pj_ctx_create_ex(const pj_system_desc* sys, int device, int options, pj_ctx*
         (e = up((void**)&c->d_sch, c->sch.data(), c->sch.size() * 4)) ||
         (e = up((void**)&c->d_seg, c->seg.data(), c->seg.size() * 4)) ||
         (e = up((void**)&c->d_segcode, c->segcode.data(), c->segcode.size() * 2)) ||
+        (e = up((void**)&c->d_segq, c->segq.data(), c->segq.size() * 4)) ||
         (e = cudaMalloc((void**)&c->d_flag, sizeof(int))) || (e = cudaMemset(c->d_flag, 0, sizeof(int)))) {
         free_ctx(c);
         cudaSetDevice(prev);

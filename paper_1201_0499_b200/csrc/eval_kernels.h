@@ -38,6 +38,9 @@ struct DevSystem {
     // staging code (j*32 + g) of the last entry of every segment, per (p, c): phase 1 leaves the
     // segment's partial in that staging slot
     const uint16_t* segcode;
+    // per (p, c, output o): {seg word, codes 0|1<<16, codes 2|3<<16, codes 4|5<<16} (first six
+    // segment codes inline)
+    const uint4* segq;
     // plain dd coefficients tiled for the fast kernel: component q of monomial
     // g = 32*chunk + lane of row p at coefT[((p*chunks + chunk)*4 + q)*32 + lane] (0 for g >= m)
     const double* coefT;
