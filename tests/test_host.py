@@ -201,3 +201,37 @@ def test_shard_range_partitions():
             assert max(b - a for a, b in rs) - min(b - a for a, b in rs) <= 1
     with pytest.raises(ValueError):
         shard_range(10, 2, 2)
+
+
+def test_newton_and_launch_argument_errors_host_only():
+    L = _lib.lib()
+    ctx = pj.EvaluationContext(pj.random_system(4, 2, 2, 2, 8), device=-1)
+    with pytest.raises(ValueError, match="host-only"):
+        ctx.newton_host(np.zeros((1, 4, 4)), "dd")
+    with pytest.raises(ValueError, match="iterations"):
+        ctx.newton_host(np.zeros((1, 4, 4)), "dd", iters=0)
+    with pytest.raises(ValueError, match="dimension"):
+        ctx.newton_host(np.zeros((1, 3, 4)), "dd")
+    with pytest.raises(ValueError, match="precision"):
+        ctx.newton_host(np.zeros((1, 4, 4)), "qd")
+    # C ABI: null buffers, negative batch, unknown precision flag; batch 0 is a no-op
+    h = ctx._h
+    assert L.pj_newton_solve(h, _lib.PJ_PREC_DD, None, None, None, 1, None, None, None, None) == _lib.PJ_EINVAL
+    assert L.pj_newton_solve(h, _lib.PJ_PREC_DD, None, None, None, -1, None, None, None, None) == _lib.PJ_EINVAL
+    assert L.pj_newton_solve(h, 7, None, None, None, 1, None, None, None, None) == _lib.PJ_EINVAL
+    assert L.pj_newton_solve(h, _lib.PJ_PREC_DD, None, None, None, 0, None, None, None, None) == _lib.PJ_OK
+    assert L.pj_newton_step(h, _lib.PJ_PREC_D, None, None, 2, None, None, None, None, None) == _lib.PJ_EINVAL
+    # launch overrides: thread counts must be multiples of 32 up to 384
+    for bad in (-32, 33, 416):
+        assert L.pj_set_launch(h, _lib.PJ_PREC_DD, bad, 0) == _lib.PJ_EINVAL
+    assert L.pj_set_kernel_variant(h, _lib.PJ_PREC_DD | _lib.PJ_ORDER_REF, 1) == _lib.PJ_EINVAL
+
+
+def test_context_options_validated():
+    s = pj.random_system(4, 2, 2, 2, 8)
+    desc, keep = s._desc()
+    h = ctypes.c_void_p()
+    assert _lib.lib().pj_ctx_create_ex(ctypes.byref(desc), -1, 0x80, ctypes.byref(h)) == _lib.PJ_EINVAL
+    assert "option" in _lib.last_error()
+    assert _lib.lib().pj_ctx_create_ex(ctypes.byref(desc), -1, _lib.PJ_CTX_WIDE, ctypes.byref(h)) == _lib.PJ_OK
+    _lib.lib().pj_ctx_destroy(h)
