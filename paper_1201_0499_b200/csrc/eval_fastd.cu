@@ -136,14 +136,17 @@ __global__ void __launch_bounds__(256, fastd_min_blocks<K>()) fastd_kernel(DevSy
                 };
                 auto SLOT = [&](int j, int u) -> double* { return stg + ((j * kP + u) * 32 + lane) * W; };
 
-                // stage 1: common factor, ref kernels.cpp:45-53 (sequential from j = 0)
+                // stage 1: common factor, ref kernels.cpp:45-53 (sequential from j = 0); for k >= 3 it
+                // runs fused with the forward products below (one gather of x_j serves both chains)
                 CD f[kP];
+                if constexpr (K <= 2) {
 #pragma unroll
-                for (int u = 0; u < kP; ++u) f[u] = PW(u, 0);
+                    for (int u = 0; u < kP; ++u) f[u] = PW(u, 0);
 #pragma unroll
-                for (int j = 1; j < K; ++j)
+                    for (int j = 1; j < K; ++j)
 #pragma unroll
-                    for (int u = 0; u < kP; ++u) f[u] = cd_mul(f[u], PW(u, j));
+                        for (int u = 0; u < kP; ++u) f[u] = cd_mul(f[u], PW(u, j));
+                }
 
                 // stage 2: speelpenning_gradient + stage2_term, ref kernels.cpp:55-127
                 if constexpr (K == 1) {
@@ -167,25 +170,41 @@ __global__ void __launch_bounds__(256, fastd_min_blocks<K>()) fastd_kernel(DevSy
                 } else {
                     // forward products L[1] = v0, L[r+2] = L[r+1] * v[r+1] (kernels.cpp:69-73); the
                     // ones the backward pass consumes are parked in their staging slots
-                    CD F[kP];
+                    // powers[pos_j][a_j - 1] given the gathered x_j
+                    auto PWv = [&](int u, int j, const CD& v) -> CD {
+                        const int e = EM1(j);
+                        if constexpr (D2) {
+                            return sel(e != 0, v, one);
+                        } else {
+                            return e == 0 ? one : ldv(xt[u] + ((e - 1) * n + POS(j)) * W);
+                        }
+                    };
+                    CD F[kP], vlast[kP];
 #pragma unroll
                     for (int u = 0; u < kP; ++u) {
-                        F[u] = X(u, 0);
-                        stv(SLOT(1, u), F[u]);
+                        const CD v0 = X(u, 0);
+                        f[u] = PWv(u, 0, v0);
+                        F[u] = v0;
+                        stv(SLOT(1, u), v0);
                     }
 #pragma unroll
-                    for (int r = 0; r + 2 <= K - 1; ++r)
+                    for (int j = 1; j < K; ++j)
 #pragma unroll
                         for (int u = 0; u < kP; ++u) {
-                            F[u] = cd_mul(F[u], X(u, r + 1));
-                            if (r + 2 < K - 1) stv(SLOT(r + 2, u), F[u]);
+                            const CD v = X(u, j);
+                            f[u] = cd_mul(f[u], PWv(u, j, v));
+                            if (j <= K - 2) {  // forward step r = j - 1: L[j+1] = L[j] * v[j]
+                                F[u] = cd_mul(F[u], v);
+                                if (j + 1 < K - 1) stv(SLOT(j + 1, u), F[u]);
+                            } else {
+                                vlast[u] = v;
+                            }
                         }
                     // backward running product (kernels.cpp:76-89), each L[j] finished in place:
                     // L[j] * factor (:108-110), then * derivative coefficient (:115-116)
-                    CD q[kP], vlast[kP];
+                    CD q[kP];
 #pragma unroll
                     for (int u = 0; u < kP; ++u) {
-                        vlast[u] = X(u, K - 1);
                         q[u] = vlast[u];
                         CD L = cd_mul(ldv(SLOT(K - 2, u)), q[u]);
                         L = cd_mul(L, f[u]);
