@@ -40,6 +40,10 @@ __device__ __forceinline__ void stv(double* p, const CD& v) { *reinterpret_cast<
 __device__ __forceinline__ CD sel(bool c, const CD& a, const CD& b) { return {c ? a.re : b.re, c ? a.im : b.im}; }
 
 constexpr int kP = 2;  // points per lane
+#ifndef PJB_FASTD_VPER
+#define PJB_FASTD_VPER 2
+#endif
+constexpr int kVPer = PJB_FASTD_VPER;  // value-chain terms per stage-3 loop iteration (measured: 2 beats 1, 4, 8)
 #ifndef PJB_FASTD_MINB
 #define PJB_FASTD_MINB(K) 2
 #endif
@@ -250,8 +254,10 @@ __global__ void __launch_bounds__(256, fastd_min_blocks<K>()) fastd_kernel(DevSy
                     CD a[kP];
 #pragma unroll
                     for (int u = 0; u < kP; ++u) a[u] = c == 0 || !jac ? zero : ldv(acc + ((v + 1) * kP + u) * W);
-                    const int vlen = v == 0 ? gl : 0;  // the value chains ride with column 0 (lane 0)
-                    const int iters = max(len, vlen);
+                    // the value chains ride with column 0 (lane 0), kVPer terms per iteration (still
+                    // one sequential chain: the loop trip count shrinks, not the order)
+                    const int vlen = v == 0 ? gl : 0;
+                    const int iters = max(len, (vlen + kVPer - 1) / kVPer);
                     for (int it = 0; it < iters; ++it) {
                         if (it < len) {
                             const int ent = __ldg(S.gm_ent + e0 + it);
@@ -259,10 +265,14 @@ __global__ void __launch_bounds__(256, fastd_min_blocks<K>()) fastd_kernel(DevSy
 #pragma unroll
                             for (int u = 0; u < kP; ++u) a[u] = cd_add(a[u], ldv(sl + u * 32 * W));
                         }
-                        if (it < vlen) {
 #pragma unroll
-                            for (int u = 0; u < kP; ++u)
-                                vacc[u] = cd_add(vacc[u], ldv(stg + ((K * kP + u) * 32 + it) * W));
+                        for (int h = 0; h < kVPer; ++h) {
+                            const int g2 = kVPer * it + h;
+                            if (g2 < vlen) {
+#pragma unroll
+                                for (int u = 0; u < kP; ++u)
+                                    vacc[u] = cd_add(vacc[u], ldv(stg + ((K * kP + u) * 32 + g2) * W));
+                            }
                         }
                     }
                     if (jac) {
