@@ -27,9 +27,9 @@
 //   x_new_i = x_i + dx_i
 //
 // B200 mapping: a CTA owns one point at a time (persistent grid over the batch). The
-// augmented matrix [J | rhs] lives in shared memory as W planes of n × (n+1) doubles (row
-// stride n+1); n ≤ 64 fits (133 KB in dd), larger systems use a per-CTA global slab with the
-// same code. Warp 0 runs one column ahead ("look-ahead"): during step kk it updates column
+// augmented matrix [J | rhs] lives in shared memory, n × (n+1) elements (row stride n+1) in the
+// pair layout (NL below); n ≤ 64 fits (133 KB in dd), larger systems use a per-CTA global slab
+// with the same code. Warp 0 runs one column ahead ("look-ahead"): during step kk it updates column
 // kk+1 of the active rows (the values stay in its registers), picks piv_{kk+1} by a redux
 // arg-max while every lane inverts its own candidates speculatively, broadcasts the winner's
 // inverse and forms the multipliers of column kk+1 and the next active-row list — while warps 1.. update columns kk+2..n of step kk (a thread keeps one pivot-row element
@@ -91,6 +91,38 @@ __device__ __forceinline__ CDD nt_inv(CDD a) {
     DD o = nt_dd_mul(re, r), p = nt_dd_mul({-a.ih, -a.il}, r);
     return {o.hi, o.lo, p.hi, p.lo};
 }
+
+// Matrix storage ("pair" layout): element e of an array of P elements keeps (re, im) at base + 2e
+// (complex double) or the high pair (re_hi, im_hi) at base + 2e and the low pair (re_lo, im_lo) at
+// base + 2P + 2e (complex dd): one 16-byte access per pair.
+template <class T>
+struct NL;
+template <>
+struct NL<CD> {
+    __device__ static CD ld(const double* A, int e, int) {
+        const double2 v = *reinterpret_cast<const double2*>(A + 2 * e);
+        return {v.x, v.y};
+    }
+    __device__ static void st(double* A, int e, int, const CD& v) {
+        *reinterpret_cast<double2*>(A + 2 * e) = make_double2(v.re, v.im);
+    }
+    // offset of AoS component comp (re, im) of element e
+    __device__ static int off(int e, int comp, int) { return 2 * e + comp; }
+};
+template <>
+struct NL<CDD> {
+    __device__ static CDD ld(const double* A, int e, int P) {
+        const double2 h = *reinterpret_cast<const double2*>(A + 2 * e);
+        const double2 l = *reinterpret_cast<const double2*>(A + 2 * P + 2 * e);
+        return {h.x, l.x, h.y, l.y};
+    }
+    __device__ static void st(double* A, int e, int P, const CDD& v) {
+        *reinterpret_cast<double2*>(A + 2 * e) = make_double2(v.rh, v.ih);
+        *reinterpret_cast<double2*>(A + 2 * P + 2 * e) = make_double2(v.rl, v.il);
+    }
+    // offset of AoS component comp (re_hi, re_lo, im_hi, im_lo) of element e
+    __device__ static int off(int e, int comp, int P) { return (comp & 1) * 2 * P + 2 * e + (comp >> 1); }
+};
 
 // dynamic shared memory ints (4 per row), rounded to whole 16-byte units, in doubles
 __host__ __device__ __forceinline__ int newton_int_words(int n) { return (4 * n + 3) / 4 * 2; }
@@ -185,33 +217,33 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
             const int idx = lane + 32 * q;
             if (idx < R) {
                 const int r = list[idx];
-                if (r != bi) S::st_planes(A + r * ld + c, P, S::mul(v[q], iv));
+                if (r != bi) NL<T>::st(A, r * ld + c, P, S::mul(v[q], iv));
                 // next list: the pivot's slot takes the last row
                 if (idx < R - 1) next[idx] = idx == bq ? list[R - 1] : r;
             }
         }
         if (lane == 0) {
-            S::st_planes(INV + c, n, iv);
+            NL<T>::st(INV, c, n, iv);
             s_piv[c] = bi;
             s_step[bi] = c;
         }
     };
     for (long long b = blockIdx.x; b < a.B; b += gridDim.x) {
         const double* ev = a.evals + size_t(b) * nout * W;
-        // ---- load [J | y − f] into planes. Shared-memory matrices: 8-byte cp.async copies straight
-        // into the planes (no registers, every copy in flight at once); global slabs: plain loads
+        // ---- load [J | y − f]. Shared-memory matrices: 8-byte cp.async copies straight into the
+        // pair layout (no registers, every copy in flight at once); global slabs: plain loads
         if (!a.gscratch) {
             for (int t = tid; t < n * n * W; t += nt) {
                 const int el = t / W, comp = t - el * W;
                 const int i = el / n, j = el - i * n;
-                const unsigned dst = unsigned(__cvta_generic_to_shared(A + size_t(comp) * P + i * ld + j));
+                const unsigned dst = unsigned(__cvta_generic_to_shared(A + NL<T>::off(i * ld + j, comp, P)));
                 asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(ev + size_t(n) * W + t));
             }
             asm volatile("cp.async.commit_group;\n" ::);
         } else {
             for (int t = tid; t < n * n; t += nt) {
                 const int i = t / n, j = t - i * n;
-                S::st_planes(A + i * ld + j, P, S::ld_aos(ev + size_t(n + t) * W));
+                NL<T>::st(A, i * ld + j, P, S::ld_aos(ev + size_t(n + t) * W));
             }
         }
         if (warp == 0) {
@@ -219,7 +251,7 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
             for (int i = lane; i < n; i += 32) {
                 T r = nt_neg(S::ld_aos(ev + size_t(i) * W));
                 if (a.target) r = S::add(S::ld_aos(a.target + (size_t(b) * n + i) * W), r);
-                S::st_planes(A + i * ld + n, P, r);
+                NL<T>::st(A, i * ld + n, P, r);
                 rn = fmax(rn, nt_magmax(r));
                 s_list0[i] = i;
             }
@@ -237,7 +269,7 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
 #pragma unroll
             for (int q = 0; q < NQ; ++q) {
                 const int idx = lane + 32 * q;
-                v[q] = idx < n ? S::ld_planes(A + idx * ld, P) : S::zero();
+                v[q] = idx < n ? NL<T>::ld(A, idx * ld, P) : S::zero();
             }
             pivot_phase(0, s_list0, n, v, s_list1);
         }
@@ -264,15 +296,15 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
             if (warp == 0) {
                 if (kk + 1 < n) {
                     const int c = kk + 1;
-                    const T u = S::ld_planes(A + pr * ld + c, P);
+                    const T u = NL<T>::ld(A, pr * ld + c, P);
                     T v[NQ];
 #pragma unroll
                     for (int q = 0; q < NQ; ++q) {
                         const int idx = lane + 32 * q;
                         if (idx < R) {
                             const int r = list[idx];
-                            v[q] = S::add(S::ld_planes(A + r * ld + c, P),
-                                          nt_neg(nt_umul(S::ld_planes(A + r * ld + kk, P), u)));
+                            v[q] = S::add(NL<T>::ld(A, r * ld + c, P),
+                                          nt_neg(nt_umul(NL<T>::ld(A, r * ld + kk, P), u)));
                         } else {
                             v[q] = S::zero();
                         }
@@ -300,17 +332,17 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
                     const int ci = c0 + (tp - rg * cw);
                     const int j1 = kk + 2 + ci, j2 = j1 + Ch;
                     const bool two = ci + Ch < Cp;
-                    const T u1 = S::ld_planes(A + pr * ld + j1, P);
-                    const T u2 = two ? S::ld_planes(A + pr * ld + j2, P) : u1;
+                    const T u1 = NL<T>::ld(A, pr * ld + j1, P);
+                    const T u2 = two ? NL<T>::ld(A, pr * ld + j2, P) : u1;
                     for (int idx = rg; idx < R; idx += G) {
                         const int r = list[idx];
-                        const T l = S::ld_planes(A + r * ld + kk, P);
-                        const T v1 = S::ld_planes(A + r * ld + j1, P);
-                        const T v2 = two ? S::ld_planes(A + r * ld + j2, P) : v1;
+                        const T l = NL<T>::ld(A, r * ld + kk, P);
+                        const T v1 = NL<T>::ld(A, r * ld + j1, P);
+                        const T v2 = two ? NL<T>::ld(A, r * ld + j2, P) : v1;
                         const T w1 = S::add(v1, nt_neg(nt_umul(l, u1)));
                         const T w2 = S::add(v2, nt_neg(nt_umul(l, u2)));
-                        S::st_planes(A + r * ld + j1, P, w1);
-                        if (two) S::st_planes(A + r * ld + j2, P, w2);
+                        NL<T>::st(A, r * ld + j1, P, w1);
+                        if (two) NL<T>::st(A, r * ld + j2, P, w2);
                     }
                 }
                 } else {
@@ -320,12 +352,12 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
                     const int G = int((unsigned(Tp) * rc) >> 16), rg = int((unsigned(tp) * rc) >> 16);
                     if (rg >= G) continue;
                     const int j = kk + 2 + c0 + (tp - rg * cw);
-                    const T u = S::ld_planes(A + pr * ld + j, P);
+                    const T u = NL<T>::ld(A, pr * ld + j, P);
                     for (int idx = rg; idx < R; idx += G) {
                         const int r = list[idx];
-                        const T l = S::ld_planes(A + r * ld + kk, P);
-                        const T v = S::ld_planes(A + r * ld + j, P);
-                        S::st_planes(A + r * ld + j, P, S::add(v, nt_neg(nt_umul(l, u))));
+                        const T l = NL<T>::ld(A, r * ld + kk, P);
+                        const T v = NL<T>::ld(A, r * ld + j, P);
+                        NL<T>::st(A, r * ld + j, P, S::add(v, nt_neg(nt_umul(l, u))));
                     }
                 }
                 }
@@ -354,7 +386,7 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) {
                     const int r = lane + 32 * q;
-                    rr[q] = r < n ? S::ld_planes(A + r * ld + n, P) : S::zero();
+                    rr[q] = r < n ? NL<T>::ld(A, r * ld + n, P) : S::zero();
                     st[q] = r < n ? s_step[r] : -1;
                 }
                 for (int s = n - 1; s >= 0; --s) {
@@ -365,18 +397,18 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
                     for (int q = 1; q < NQ; ++q)
                         if (q == qi) xs = rr[q];
                     xs = shfl_idx(xs, owner);
-                    xs = S::mul(xs, S::ld_planes(INV + s, n));
-                    if (lane == 0) S::st_planes(DX + s, n, xs);
+                    xs = S::mul(xs, NL<T>::ld(INV, s, n));
+                    if (lane == 0) NL<T>::st(DX, s, n, xs);
 #pragma unroll
                     for (int q = 0; q < NQ; ++q)
                         if (st[q] >= 0 && st[q] < s)
-                            rr[q] = S::add(rr[q], nt_neg(nt_umul(S::ld_planes(A + (lane + 32 * q) * ld + s, P), xs)));
+                            rr[q] = S::add(rr[q], nt_neg(nt_umul(NL<T>::ld(A, (lane + 32 * q) * ld + s, P), xs)));
                 }
                 __syncwarp();
                 double dn = 0.0;
                 bool fin = true;
                 for (int i = lane; i < n; i += 32) {
-                    const T d = S::ld_planes(DX + i, n);
+                    const T d = NL<T>::ld(DX, i, n);
                     const T xn = S::add(S::ld_aos(x + size_t(i) * W), d);
                     S::st_aos(xo + size_t(i) * W, xn);
                     dn = fmax(dn, nt_magmax(d));
