@@ -170,9 +170,17 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
     double* DX = INV + size_t(W) * n;   // [W][n] solution
     const size_t nout = size_t(n) * n + n;
 
+#ifdef PJB_NT_TRACE
+    long long* tsub = nullptr;  // look-ahead sub-phase clocks (developer instrumentation)
+#define PJB_TSUB(c, k) \
+    if (tsub && lane == 0) tsub[4 * (c) + (k)] = clock64();
+#else
+#define PJB_TSUB(c, k)
+#endif
     // Warp-0 look-ahead for column c: rows list[0..R) (values v[] already in registers), pick the
     // pivot, store inv_c and the multipliers of column c, write the next list (R-1 rows).
     auto pivot_phase = [&](int c, const int* list, int R, const T* v, int* next) {
+        PJB_TSUB(c, 0)
         // every lane inverts its own candidates speculatively, off the arg-max's critical path
         T ivq[NQ];
 #pragma unroll
@@ -200,6 +208,7 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
         const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
         const bool cand = bi >= 0 && hi == mh && lo == ml;
         const int rmin = __reduce_min_sync(0xffffffffu, cand ? bi : 0x7fffffff);
+        PJB_TSUB(c, 1)
         if (rmin == 0x7fffffff) {
             if (lane == 0) s_sing = 1;
             return;
@@ -212,6 +221,7 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
         for (int q = 1; q < NQ; ++q)
             if (q == (bq >> 5)) iv = ivq[q];
         iv = shfl_idx(iv, owner);
+        PJB_TSUB(c, 2)
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
             const int idx = lane + 32 * q;
@@ -227,6 +237,7 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
             s_piv[c] = bi;
             s_step[bi] = c;
         }
+        PJB_TSUB(c, 3)
     };
     for (long long b = blockIdx.x; b < a.B; b += gridDim.x) {
         const double* ev = a.evals + size_t(b) * nout * W;
@@ -284,6 +295,7 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
         // (the trace lives after the B status words: status must have B + 2 + 8n entries)
         long long* trace = (blockIdx.x == 0 && b == 0 && a.status)
                                ? reinterpret_cast<long long*>(a.status + ((a.B + 1) & ~1LL)) : nullptr;
+        tsub = trace ? trace + 4 * n : nullptr;
 #endif
         for (int kk = 0; kk < n && !singular; ++kk) {
 #ifdef PJB_NT_TRACE

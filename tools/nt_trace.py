@@ -18,14 +18,20 @@ for B in [65536, 1]:
     ctx.evaluate_device(x, work, "dd")
     out = torch.empty_like(x)
     off = (B + 1) & ~1
-    tr = torch.zeros(off + 8 * n, dtype=torch.int32, device="cuda")  # statuses, then 8-byte trace entries
+    tr = torch.zeros(off + 16 * n, dtype=torch.int32, device="cuda")  # statuses, then 8-byte trace entries
     import ctypes
     from paper_1201_0499_b200 import _lib
     nr = torch.empty((B, 2), dtype=torch.float64, device="cuda")
     _lib.check(_lib.lib().pj_newton_solve(ctx._h, _lib.PJ_PREC_DD, work.data_ptr(), x.data_ptr(), None, B,
                                           out.data_ptr(), nr.data_ptr(), tr.data_ptr(), None))
     torch.cuda.synchronize()
-    t = tr[off:].cpu().numpy().view(np.int64)[: 4 * n].reshape(n, 4)
+    tt = tr[off:].cpu().numpy().view(np.int64)
+    t = tt[: 4 * n].reshape(n, 4)
+    sub = tt[4 * n: 8 * n].reshape(n, 4)
+    d = np.diff(sub[1:n - 1], axis=1)  # columns 1..n-2: update -> argmax, argmax -> inverse, -> end
+    print(f"B={B}: look-ahead sub-phases (cycles, mean over columns): column update+argmax {d[:, 0].mean():.0f}, "
+          f"inverse broadcast {d[:, 1].mean():.0f}, multipliers+list {d[:, 2].mean():.0f}; "
+          f"step start -> look-ahead entry {np.mean(sub[1:n - 1, 0] - t[0:n - 2, 0]):.0f}")
     t0 = t[0, 0]
     la = t[:, 2] - t[:, 0]
     upd = t[:, 3] - t[:, 1]
