@@ -419,6 +419,11 @@ def main():
         nst = torch.empty(B, dtype=torch.int32, device=dev)
         ms_solve = timed(lambda: ctx.newton_solve_device(out, bufs[0], xo, "dd", status=nst, stream=stream), 5)
         ms_step = timed(lambda: ctx.newton_step_device(bufs[0], out, xo, "dd", status=nst, stream=stream), 5)
+        # end to end through the host API: points in, corrected points out (1 KB each way per point)
+        ctx.newton_host(dd, "dd", iters=1)  # warm (allocates the staging buffers)
+        t0 = time.perf_counter()
+        ctx.newton_host(dd, "dd", iters=1)
+        e2e_newton_s = time.perf_counter() - t0
         nf = newton_model_flops(N)
         line["newton"] = {"config": "f1: C2 Newton step x <- x + J^-1 (-f), complex dd, 65,536 points per GPU",
                           "steps_per_s": B / (ms_step * 1e-3), "ms_per_step": ms_step,
@@ -426,6 +431,9 @@ def main():
                           "solve_flops_per_point": nf,
                           "solve_fp64_frac": nf * B / (ms_solve * 1e-3) / 1e12 / peak,
                           "status_ok_frac": float((nst == 0).float().mean().item()),
+                          "e2e_steps_per_s": B / e2e_newton_s,
+                          "e2e_api": "EvaluationContext.newton_host -> pj_newton_host (H2D points, evaluate + solve "
+                                     "in L2-sized chunks, D2H corrected points, norms, status)",
                           "launch": ctx.launch("dd", newton=True)}
         del xo
 
