@@ -238,9 +238,6 @@ __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) f
                 }
                 st_hl(SLOT(0), 64, SCALE(0, q));
                 __syncwarp();
-#ifdef PJB_EXP_NO_STAGE3
-                if (codes[0] != 0xdeadbeefu) continue;  // experiment: stage 2 only
-#endif
                 // ---- stage 3, phase 1: balanced segmented sums. The (row, chunk) schedule
                 // hands every lane R consecutive entries of the output-major, ascending-g list
                 // of staged terms; a lane flushes its running sum at segment ends. The running

@@ -15,9 +15,6 @@ import torch
 import paper_1201_0499_b200 as pj
 from oracle import oracle as O
 
-FV = lambda P, SH, FREG: (P << 2) | (FREG << 1) | SH
-
-
 def model_flops(n, m, k, d):
     return (n * max(d - 2, 0) + n * m * (k - 1) + n * m * (5 * k - 4)) * 80 + n * m * (k + 1) * 40
 
