@@ -40,6 +40,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <mutex>
+#include <set>
 
 #include "dd.cuh"
 #include "eval_kernels.h"
@@ -458,14 +460,20 @@ size_t newton_matrix_bytes(int prec, int n) {
 }
 size_t newton_int_bytes(int n) { return size_t(newton_int_words(n)) * sizeof(double); }
 
+// The reciprocal table is __constant__ memory: one copy per device, filled once per device
+// (thread-safe: contexts on several devices may launch concurrently).
 static cudaError_t init_recip() {
-    static bool done = false;
-    if (done) return cudaSuccess;
+    static std::mutex mu;
+    static std::set<int> ready;
+    int dev = 0;
+    if (cudaError_t e = cudaGetDevice(&dev)) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (ready.count(dev)) return cudaSuccess;
     unsigned h[257];
     h[0] = 0;
     for (int c = 1; c <= 256; ++c) h[c] = (65536u + c - 1) / c;
     cudaError_t e = cudaMemcpyToSymbol(kRecip, h, sizeof(h));
-    if (e == cudaSuccess) done = true;
+    if (e == cudaSuccess) ready.insert(dev);
     return e;
 }
 
