@@ -345,3 +345,29 @@ def test_dd_contract_under_cancellation(gpu):
     p4 = stress_dd(unit, 6)
     want, ms = O.evaluate("dd", S2, p4, magsum=True)
     assert dd_rel(c2.evaluate_dd(p4), want, ms) <= DD_TOL
+
+
+def test_distinct_contexts_are_thread_safe(gpu):
+    # ref engine.hpp:84-86: one context per thread; distinct contexts may run concurrently
+    import threading
+    systems = [pj.random_system(32, 32, 8, 2, 900 + i) for i in range(3)]
+    pts = [stress_dd(pj.random_points(32, 257, 910 + i), i) for i in range(3)]
+    want = [pj.EvaluationContext(s).evaluate_dd(p) for s, p in zip(systems, pts)]
+    want_x = [pj.EvaluationContext(s).newton_host(p, "dd")[0] for s, p in zip(systems, pts)]
+    errors = []
+
+    def work(i):
+        try:
+            ctx = pj.EvaluationContext(systems[i])
+            for _ in range(4):
+                assert np.array_equal(ctx.evaluate_dd(pts[i]).view(np.uint64), want[i].view(np.uint64))
+                assert np.array_equal(ctx.newton_host(pts[i], "dd")[0].view(np.uint64), want_x[i].view(np.uint64))
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(3)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
