@@ -419,10 +419,15 @@ def main():
         nst = torch.empty(B, dtype=torch.int32, device=dev)
         ms_solve = timed(lambda: ctx.newton_solve_device(out, bufs[0], xo, "dd", status=nst, stream=stream), 5)
         ms_step = timed(lambda: ctx.newton_step_device(bufs[0], out, xo, "dd", status=nst, stream=stream), 5)
-        # end to end through the host API: points in, corrected points out (1 KB each way per point)
-        ctx.newton_host(dd, "dd", iters=1)  # warm (allocates the staging buffers)
+        # end to end through the host API: points in, corrected points out (1 KB each way per point),
+        # page-locked host buffers
+        hx = torch.from_numpy(dd).pin_memory().numpy()
+        hxo = torch.empty(dd.shape, dtype=torch.float64).pin_memory().numpy()
+        hn = torch.empty((B, 2), dtype=torch.float64).pin_memory().numpy()
+        hs = torch.empty(B, dtype=torch.int32).pin_memory().numpy()
+        ctx.newton_host(hx, "dd", iters=1, out=hxo, norms=hn, status=hs)  # warm (allocates staging)
         t0 = time.perf_counter()
-        ctx.newton_host(dd, "dd", iters=1)
+        ctx.newton_host(hx, "dd", iters=1, out=hxo, norms=hn, status=hs)
         e2e_newton_s = time.perf_counter() - t0
         nf = newton_model_flops(N)
         line["newton"] = {"config": "f1: C2 Newton step x <- x + J^-1 (-f), complex dd, 65,536 points per GPU",

@@ -157,8 +157,9 @@ struct pj_ctx {
     } newton[2];
     double* d_nscratch = nullptr;
     size_t nscratch_bytes = 0;
-    double *d_nx = nullptr, *d_nwork = nullptr, *d_ntgt = nullptr, *d_nnorm = nullptr;
-    int* d_nstat = nullptr;
+    double *d_nx[kHostStreams] = {}, *d_nwork[kHostStreams] = {}, *d_ntgt[kHostStreams] = {},
+           *d_nnorm[kHostStreams] = {};
+    int* d_nstat[kHostStreams] = {};
     size_t nx_cap = 0, nwork_cap = 0;
 
     pjb::DevSystem dev(int pi) const {
@@ -210,11 +211,13 @@ void free_ctx(pj_ctx* c) {
     cudaFree(c->d_coefT);
     cudaFree(c->d_scratch);
     cudaFree(c->d_nscratch);
-    cudaFree(c->d_nx);
-    cudaFree(c->d_nwork);
-    cudaFree(c->d_ntgt);
-    cudaFree(c->d_nnorm);
-    cudaFree(c->d_nstat);
+    for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
+        cudaFree(c->d_nx[i]);
+        cudaFree(c->d_nwork[i]);
+        cudaFree(c->d_ntgt[i]);
+        cudaFree(c->d_nnorm[i]);
+        cudaFree(c->d_nstat[i]);
+    }
     for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
         cudaFree(c->d_in[i]);
         cudaFree(c->d_out[i]);
@@ -1043,56 +1046,70 @@ int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double*
     const int W = pi == 0 ? 2 : 4;
     const size_t x_pt = size_t(ctx->n) * W * 8;
     const size_t out_pt = (size_t(ctx->n) * ctx->n + ctx->n) * W * 8;
-    // chunk: the evaluator's output for one chunk stays L2-resident (<= 96 MiB) between the
-    // evaluation and the solve; whole evaluation waves when the chunk spans more than one
+    // chunks of whole evaluation waves (>= 4 waves, >= 96 MiB of evaluator output), pipelined over
+    // the context's host streams: each stream owns one set of staging buffers, so the H2D of one
+    // chunk, the evaluate + solve of another and the D2H of a third overlap (stream order protects
+    // every buffer's reuse)
     const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
     const int64_t wave = std::max<int64_t>(int64_t(L.blocks) * L.tp, 1);
-    int64_t chunk = std::max<int64_t>(int64_t((96ull << 20) / out_pt), 1);
+    int64_t chunk = std::max<int64_t>(std::max<int64_t>(int64_t((96ull << 20) / out_pt), 4 * wave), 1);
     if (chunk > wave) chunk = chunk / wave * wave;
     chunk = std::min<int64_t>(chunk, batch);
+    const int nchunks = int((batch + chunk - 1) / chunk);
+    const int ns = std::min(nchunks, int(pj_ctx::kHostStreams));
     int prev = 0;
     cudaGetDevice(&prev);
     PJ_CUDA(cudaSetDevice(ctx->device));
     if (size_t(chunk) * x_pt > ctx->nx_cap || size_t(chunk) * out_pt > ctx->nwork_cap) {
-        cudaFree(ctx->d_nx);
-        cudaFree(ctx->d_nwork);
-        cudaFree(ctx->d_ntgt);
-        cudaFree(ctx->d_nnorm);
-        cudaFree(ctx->d_nstat);
-        ctx->d_nx = ctx->d_nwork = ctx->d_ntgt = ctx->d_nnorm = nullptr;
-        ctx->d_nstat = nullptr;
+        for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
+            cudaFree(ctx->d_nx[i]);
+            cudaFree(ctx->d_nwork[i]);
+            cudaFree(ctx->d_ntgt[i]);
+            cudaFree(ctx->d_nnorm[i]);
+            cudaFree(ctx->d_nstat[i]);
+            ctx->d_nx[i] = ctx->d_nwork[i] = ctx->d_ntgt[i] = ctx->d_nnorm[i] = nullptr;
+            ctx->d_nstat[i] = nullptr;
+        }
         ctx->nx_cap = ctx->nwork_cap = 0;
-        PJ_CUDA(cudaMalloc(&ctx->d_nx, size_t(chunk) * x_pt));
-        PJ_CUDA(cudaMalloc(&ctx->d_ntgt, size_t(chunk) * x_pt));
-        PJ_CUDA(cudaMalloc(&ctx->d_nwork, size_t(chunk) * out_pt));
-        PJ_CUDA(cudaMalloc(&ctx->d_nnorm, size_t(chunk) * 2 * sizeof(double)));
-        PJ_CUDA(cudaMalloc(&ctx->d_nstat, size_t(chunk) * sizeof(int32_t)));
+        for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
+            PJ_CUDA(cudaMalloc(&ctx->d_nx[i], size_t(chunk) * x_pt));
+            PJ_CUDA(cudaMalloc(&ctx->d_ntgt[i], size_t(chunk) * x_pt));
+            PJ_CUDA(cudaMalloc(&ctx->d_nwork[i], size_t(chunk) * out_pt));
+            PJ_CUDA(cudaMalloc(&ctx->d_nnorm[i], size_t(chunk) * 2 * sizeof(double)));
+            PJ_CUDA(cudaMalloc(&ctx->d_nstat[i], size_t(chunk) * sizeof(int32_t)));
+        }
         ctx->nx_cap = size_t(chunk) * x_pt;
         ctx->nwork_cap = size_t(chunk) * out_pt;
     }
-    cudaStream_t st = ctx->hstream[0];
     int rc = PJ_OK;
-    for (int64_t b0 = 0; b0 < batch && rc == PJ_OK; b0 += chunk) {
-        const int64_t nb = std::min<int64_t>(chunk, batch - b0);
-        PJ_CUDA(cudaMemcpyAsync(ctx->d_nx, reinterpret_cast<const char*>(h_points) + size_t(b0) * x_pt,
-                                size_t(nb) * x_pt, cudaMemcpyHostToDevice, st));
-        if (h_target)
-            PJ_CUDA(cudaMemcpyAsync(ctx->d_ntgt, reinterpret_cast<const char*>(h_target) + size_t(b0) * x_pt,
+    for (int c = 0; c < nchunks && rc == PJ_OK; ++c) {
+        const int si = c % ns;
+        cudaStream_t st = ctx->hstream[si];
+        const int64_t b0 = int64_t(c) * chunk, nb = std::min<int64_t>(chunk, batch - b0);
+        double* dx = ctx->d_nx[si];
+        double* dt = h_target ? ctx->d_ntgt[si] : nullptr;
+        PJ_CUDA(cudaMemcpyAsync(dx, reinterpret_cast<const char*>(h_points) + size_t(b0) * x_pt, size_t(nb) * x_pt,
+                                cudaMemcpyHostToDevice, st));
+        if (dt)
+            PJ_CUDA(cudaMemcpyAsync(dt, reinterpret_cast<const char*>(h_target) + size_t(b0) * x_pt,
                                     size_t(nb) * x_pt, cudaMemcpyHostToDevice, st));
         for (int it = 0; it < iters && rc == PJ_OK; ++it)
-            rc = pj_newton_step(ctx, flags, ctx->d_nx, h_target ? ctx->d_ntgt : nullptr, nb, ctx->d_nwork, ctx->d_nx,
-                                ctx->d_nnorm, ctx->d_nstat, st);
+            rc = pj_newton_step(ctx, flags, dx, dt, nb, ctx->d_nwork[si], dx, ctx->d_nnorm[si], ctx->d_nstat[si], st);
         if (rc) break;
-        PJ_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(h_points_out) + size_t(b0) * x_pt, ctx->d_nx,
-                                size_t(nb) * x_pt, cudaMemcpyDeviceToHost, st));
+        PJ_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(h_points_out) + size_t(b0) * x_pt, dx, size_t(nb) * x_pt,
+                                cudaMemcpyDeviceToHost, st));
         if (h_norms)
-            PJ_CUDA(cudaMemcpyAsync(h_norms + 2 * b0, ctx->d_nnorm, size_t(nb) * 2 * sizeof(double),
+            PJ_CUDA(cudaMemcpyAsync(h_norms + 2 * b0, ctx->d_nnorm[si], size_t(nb) * 2 * sizeof(double),
                                     cudaMemcpyDeviceToHost, st));
         if (h_status)
-            PJ_CUDA(cudaMemcpyAsync(h_status + b0, ctx->d_nstat, size_t(nb) * sizeof(int32_t), cudaMemcpyDeviceToHost,
-                                    st));
-        PJ_CUDA(cudaStreamSynchronize(st));  // the staging buffers are reused by the next chunk
+            PJ_CUDA(cudaMemcpyAsync(h_status + b0, ctx->d_nstat[si], size_t(nb) * sizeof(int32_t),
+                                    cudaMemcpyDeviceToHost, st));
     }
+    for (int i = 0; i < ns; ++i) {
+        cudaError_t e = cudaStreamSynchronize(ctx->hstream[i]);
+        if (e && rc == PJ_OK) rc = cuda_fail(e, "newton_host: stream");
+    }
+    cudaStream_t st = ctx->hstream[0];
     if (rc) {
         cudaSetDevice(prev);
         return rc;

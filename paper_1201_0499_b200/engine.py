@@ -424,11 +424,13 @@ class EvaluationContext:
 
     # ---- Newton corrector (csrc/newton.cu)
     def newton_host(self, points: np.ndarray, precision: str = "dd", iters: int = 1, target: np.ndarray | None = None,
-                    order: str | None = None):
+                    order: str | None = None, out: np.ndarray | None = None, norms: np.ndarray | None = None,
+                    status: np.ndarray | None = None):
         """`iters` Newton steps x <- x + J(x)^-1 (y - f(x)) per point, on the GPU.
         points (and target y, optional; absent = the roots of f): [B, n, W] float64.
         Returns (points_out [B, n, W], norms [B, 2] = max-norms of y - f and of the last step,
-        status [B] int32: 0 ok, 1 singular Jacobian, 2 non-finite result)."""
+        status [B] int32: 0 ok, 1 singular Jacobian, 2 non-finite result). out / norms / status may be
+        preallocated (page-locked buffers give full H2D / compute / D2H overlap)."""
         W = 2 if precision == "d" else 4
         pts = np.ascontiguousarray(points, np.float64)
         if pts.ndim != 3 or pts.shape[1:] != (self.n, W):
@@ -439,9 +441,15 @@ class EvaluationContext:
             if tg.shape != pts.shape:
                 raise ValueError("newton: target shape mismatch")
         B = pts.shape[0]
-        out = np.empty_like(pts)
-        norms = np.empty((B, 2), np.float64)
-        status = np.empty(B, np.int32)
+        if out is None:
+            out = np.empty_like(pts)
+        if norms is None:
+            norms = np.empty((B, 2), np.float64)
+        if status is None:
+            status = np.empty(B, np.int32)
+        for a, shp, dt in ((out, pts.shape, np.float64), (norms, (B, 2), np.float64), (status, (B,), np.int32)):
+            if a.shape != shp or a.dtype != dt or not a.flags.c_contiguous:
+                raise ValueError("newton: output buffer must be C-contiguous %s of shape %s" % (np.dtype(dt), shp))
         check(lib().pj_newton_host(self._h, _flags(precision, order), pts.ctypes.data,
                                    tg.ctypes.data if tg is not None else None, B, iters, out.ctypes.data,
                                    norms.ctypes.data, status.ctypes.data))
