@@ -148,6 +148,7 @@ struct pj_ctx {
     size_t in_cap = 0, out_cap = 0;
     cudaStream_t hstream[kHostStreams] = {};
     cudaEvent_t hdone[kHostStreams] = {};
+    cudaEvent_t nfork = nullptr;  // pj_newton_step fork event
     // Newton corrector (f1): launch shape per precision, global matrix slabs when the
     // augmented matrix exceeds shared memory, host-API staging buffers
     struct NewtonPlan {
@@ -224,6 +225,7 @@ void free_ctx(pj_ctx* c) {
         if (c->hstream[i]) cudaStreamDestroy(c->hstream[i]);
         if (c->hdone[i]) cudaEventDestroy(c->hdone[i]);
     }
+    if (c->nfork) cudaEventDestroy(c->nfork);
     cudaSetDevice(prev);
     delete c;
 }
@@ -1022,12 +1024,63 @@ int pj_newton_solve(pj_ctx* ctx, int flags, const double* d_evals, const double*
     return PJ_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// evaluate + solve of one batch on one stream
+int newton_step_on(pj_ctx* ctx, int flags, const double* d_points, const double* d_target, int64_t batch,
+                   double* d_work, double* d_points_out, double* d_norms, int32_t* d_status, cudaStream_t st) {
+    if (batch > 0 && !d_work) return fail(PJ_EINVAL, "newton: null buffer");
+    int rc = pj_evaluate(ctx, flags, d_points, batch, d_work, st);
+    if (rc) return rc;
+    return pj_newton_solve(ctx, flags, d_work, d_points, d_target, batch, d_points_out, d_norms, d_status, st);
+}
+}  // namespace
+
+extern "C" {
+
 int pj_newton_step(pj_ctx* ctx, int flags, const double* d_points, const double* d_target, int64_t batch,
                    double* d_work, double* d_points_out, double* d_norms, int32_t* d_status, void* stream) {
-    if (batch > 0 && !d_work) return fail(PJ_EINVAL, "newton: null buffer");
-    int rc = pj_evaluate(ctx, flags, d_points, batch, d_work, stream);
-    if (rc) return rc;
-    return pj_newton_solve(ctx, flags, d_work, d_points, d_target, batch, d_points_out, d_norms, d_status, stream);
+    if (!ctx) return fail(PJ_EINVAL, "null context");
+    const int pi = prec_index(flags);
+    if (pi < 0) return fail(PJ_EINVAL, "newton: unknown precision flag");
+    if (batch <= 0 || ctx->host_only || !d_points || !d_work || !d_points_out)
+        return newton_step_on(ctx, flags, d_points, d_target, batch, d_work, d_points_out, d_norms, d_status,
+                              (cudaStream_t)stream);
+    // Large batches: chunks of >= 4 evaluation waves alternate over two of the context's streams
+    // (fork/join with events on the caller's stream), so one chunk's solve (latency-bound)
+    // overlaps the next chunk's evaluation (FP64-bound). Chunks are independent point ranges.
+    const int W = pi == 0 ? 2 : 4;
+    const size_t x_pt = size_t(ctx->n) * W, out_pt = (size_t(ctx->n) * ctx->n + ctx->n) * W;  // doubles
+    const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
+    const int64_t chunk = std::max<int64_t>(int64_t(L.blocks) * L.tp * 4, 1);
+    if (batch < 2 * chunk)
+        return newton_step_on(ctx, flags, d_points, d_target, batch, d_work, d_points_out, d_norms, d_status,
+                              (cudaStream_t)stream);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != ctx->device) PJ_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t user = (cudaStream_t)stream;
+    cudaError_t e = cudaSuccess;
+    if (!ctx->nfork) e = cudaEventCreateWithFlags(&ctx->nfork, cudaEventDisableTiming);
+    if (!e) e = cudaEventRecord(ctx->nfork, user);
+    for (int s = 0; s < 2 && !e; ++s) e = cudaStreamWaitEvent(ctx->hstream[s], ctx->nfork, 0);
+    int rc = e ? cuda_fail(e, "newton_step: fork") : PJ_OK;
+    const int nchunks = int((batch + chunk - 1) / chunk);
+    for (int c = 0; c < nchunks && rc == PJ_OK; ++c) {
+        const int64_t b0 = int64_t(c) * chunk, nb = std::min<int64_t>(chunk, batch - b0);
+        rc = newton_step_on(ctx, flags, d_points + b0 * x_pt, d_target ? d_target + b0 * x_pt : nullptr, nb,
+                            d_work + b0 * out_pt, d_points_out + b0 * x_pt, d_norms ? d_norms + 2 * b0 : nullptr,
+                            d_status ? d_status + b0 : nullptr, ctx->hstream[c & 1]);
+    }
+    for (int s = 0; s < 2; ++s) {  // join (also after a failure: the caller's stream must not run ahead)
+        cudaError_t e2 = cudaEventRecord(ctx->hdone[s], ctx->hstream[s]);
+        if (!e2) e2 = cudaStreamWaitEvent(user, ctx->hdone[s], 0);
+        if (e2 && rc == PJ_OK) rc = cuda_fail(e2, "newton_step: join");
+    }
+    if (prev != ctx->device) cudaSetDevice(prev);
+    if (rc == PJ_OK) g_err.clear();
+    return rc;
 }
 
 int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double* h_target, int64_t batch, int iters,
@@ -1094,7 +1147,7 @@ int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double*
             PJ_CUDA(cudaMemcpyAsync(dt, reinterpret_cast<const char*>(h_target) + size_t(b0) * x_pt,
                                     size_t(nb) * x_pt, cudaMemcpyHostToDevice, st));
         for (int it = 0; it < iters && rc == PJ_OK; ++it)
-            rc = pj_newton_step(ctx, flags, dx, dt, nb, ctx->d_nwork[si], dx, ctx->d_nnorm[si], ctx->d_nstat[si], st);
+            rc = newton_step_on(ctx, flags, dx, dt, nb, ctx->d_nwork[si], dx, ctx->d_nnorm[si], ctx->d_nstat[si], st);
         if (rc) break;
         PJ_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(h_points_out) + size_t(b0) * x_pt, dx, size_t(nb) * x_pt,
                                 cudaMemcpyDeviceToHost, st));

@@ -166,3 +166,23 @@ def test_step_device_in_place_and_errors(gpu):
     bad[3, 4, 0] = np.nan
     with pytest.raises(ValueError):
         ctx.newton_host(bad, "dd")
+
+
+def test_step_device_chunked_fork_join(gpu):
+    # batches of >= 2 chunks (4 evaluation waves each) run over two internal streams with
+    # fork/join events on the caller's stream: same bits as the oracle, in place, on a side stream
+    import torch
+    s, S, pts = shaped(32, 32, 8, 2, 9000)
+    ctx = pj.EvaluationContext(s)
+    p = pj.to_dd(pts)
+    x = torch_dev(p)
+    work = torch.empty((9000, 32 + 32 * 32, 4), dtype=torch.float64, device="cuda")
+    st = torch.empty(9000, dtype=torch.int32, device="cuda")
+    side = torch.cuda.Stream()
+    with torch.cuda.stream(side):
+        ctx.newton_step_device(x, work, x, "dd", order="ref", status=st, stream=side)
+        x2 = x.clone()  # ordered after the join on the caller's stream
+    side.synchronize()
+    want, _, wst = O.newton_solve("dd", 32, O.evaluate("dd", S, p, threads=8), p, threads=8)
+    assert np.array_equal(x2.cpu().numpy().view(np.uint64), want.view(np.uint64))
+    assert np.array_equal(st.cpu().numpy(), wst)
