@@ -708,6 +708,8 @@ int pj_evaluate_host(pj_ctx* ctx, int flags, const double* h_points, int64_t bat
     const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
     int64_t chunk = std::max<int64_t>(int64_t(L.blocks) * L.tp * 4, 1024);
     chunk = std::max<int64_t>(chunk, int64_t((256ull << 20) / out_pt));
+    // bounded staging: at most ~1 GiB of results per stream (wide systems have MB-sized results)
+    chunk = std::min<int64_t>(chunk, std::max<int64_t>(1, int64_t((1ull << 30) / out_pt)));
     chunk = std::min<int64_t>(chunk, batch);
     const int nchunks = int((batch + chunk - 1) / chunk);
     const int ns = std::min(nchunks, int(pj_ctx::kHostStreams));
@@ -1107,6 +1109,7 @@ int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double*
     const int64_t wave = std::max<int64_t>(int64_t(L.blocks) * L.tp, 1);
     int64_t chunk = std::max<int64_t>(std::max<int64_t>(int64_t((96ull << 20) / out_pt), 4 * wave), 1);
     if (chunk > wave) chunk = chunk / wave * wave;
+    chunk = std::min<int64_t>(chunk, std::max<int64_t>(1, int64_t((1ull << 30) / out_pt)));  // bounded staging
     chunk = std::min<int64_t>(chunk, batch);
     const int nchunks = int((batch + chunk - 1) / chunk);
     const int ns = std::min(nchunks, int(pj_ctx::kHostStreams));
