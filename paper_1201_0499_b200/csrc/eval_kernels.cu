@@ -9,7 +9,7 @@
 //
 // Mapping (B200-first):
 //   * a CTA owns a tile of TP points; their coordinates (and for d > 2 the power table
-//     x_v^e, e = 1..d-1, ref kernels.cpp:16-24) sit in shared memory in plane layout;
+//     x_v^e, e = 1..d-1, ref kernels.cpp:16-24) sit in shared memory in pair layout (ld_pr);
 //   * a warp owns one (polynomial row p, point) task at a time; lane g evaluates monomial
 //     g of row p (stages 1 and 2 in registers; the forward products of the Speelpenning
 //     schedule are parked in the warp's staging area, which then receives the k+1 final
@@ -33,6 +33,26 @@
 
 namespace pjb {
 
+// Pair layout (like the fast kernels): element e of an array of P elements keeps (re, im) at
+// base + 2e (complex double) or (re_hi, im_hi) at base + 2e and (re_lo, im_lo) at base + 2P + 2e
+// (complex dd) — one 16-byte shared access per pair.
+__device__ __forceinline__ CD ld_pr(const double* base, int e, int, CD*) {
+    const double2 v = *reinterpret_cast<const double2*>(base + 2 * e);
+    return {v.x, v.y};
+}
+__device__ __forceinline__ CDD ld_pr(const double* base, int e, int P, CDD*) {
+    const double2 h = *reinterpret_cast<const double2*>(base + 2 * e);
+    const double2 l = *reinterpret_cast<const double2*>(base + 2 * P + 2 * e);
+    return {h.x, l.x, h.y, l.y};
+}
+__device__ __forceinline__ void st_pr(double* base, int e, int, const CD& v) {
+    *reinterpret_cast<double2*>(base + 2 * e) = make_double2(v.re, v.im);
+}
+__device__ __forceinline__ void st_pr(double* base, int e, int P, const CDD& v) {
+    *reinterpret_cast<double2*>(base + 2 * e) = make_double2(v.rh, v.ih);
+    *reinterpret_cast<double2*>(base + 2 * P + 2 * e) = make_double2(v.rl, v.il);
+}
+
 constexpr int kRef = 0;
 constexpr int kFast = 1;
 
@@ -42,9 +62,10 @@ __global__ void __launch_bounds__(256) eval_kernel(DevSystem S, const double* __
                                                    double* __restrict__ gscratch, int* __restrict__ flag) {
     using O = Sc<T>;
     constexpr int W = O::W;
-    extern __shared__ double smem_[];
+    extern __shared__ __align__(16) double smem_[];
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = S.n, k = S.k, m = S.m, d = S.d;
+    auto LD = [](const double* base, int e, int P) -> T { return ld_pr(base, e, P, static_cast<T*>(nullptr)); };
     const int D1 = d > 2 ? d - 1 : 1;  // stored powers e = 1..D1
     const int tabPt = D1 * W * n;      // doubles per point
     const int stgW = (k + 1) * W * 32;  // staging doubles per warp
@@ -65,18 +86,18 @@ __global__ void __launch_bounds__(256) eval_kernel(DevSystem S, const double* __
             const int t = i / n, v = i - t * n;
             T x = O::ld_aos(pts + ((b0 + t) * n + v) * W);
             if (!O::finite(x)) atomicOr(flag, 1);
-            O::st_planes(tab + t * tabPt + v, n, x);
+            st_pr(tab + t * tabPt, v, n, x);
         }
         __syncthreads();
         if (d > 2) {  // power chains, ref kernels.cpp:16-24: row[e] = row[e-1] * x
             for (int i = threadIdx.x; i < tp * n; i += blockDim.x) {
                 const int t = i / n, v = i - t * n;
-                double* pb = tab + t * tabPt + v;
-                const T x = O::ld_planes(pb, n);
+                double* pb = tab + t * tabPt;
+                const T x = LD(pb, v, n);
                 T r = x;
                 for (int e = 2; e < d; ++e) {
                     r = O::mul(r, x);
-                    O::st_planes(pb + (e - 1) * W * n, n, r);
+                    st_pr(pb + (e - 1) * W * n, v, n, r);
                 }
             }
             __syncthreads();
@@ -98,11 +119,11 @@ __global__ void __launch_bounds__(256) eval_kernel(DevSystem S, const double* __
                     const double* cf = S.coef + s;
                     auto POS = [&](int j) -> int { return wide ? int(__ldg(pe32 + j) & 0xffffu) : (__ldg(pe + j) & 255); };
                     auto EXP = [&](int j) -> int { return wide ? int(__ldg(pe32 + j) >> 16) : (__ldg(pe + j) >> 8); };
-                    auto X = [&](int j) -> T { return O::ld_planes(xt + POS(j), n); };
+                    auto X = [&](int j) -> T { return LD(xt, POS(j), n); };
                     auto PW = [&](int j) -> T {
                         const int e = EXP(j);
                         if (e == 0) return O::one();
-                        return O::ld_planes(xt + (e - 1) * W * n + POS(j), n);
+                        return LD(xt + (e - 1) * W * n, POS(j), n);
                     };
                     auto COEF = [&](int j) -> T {
                         const double* q = cf + (size_t)j * W * nm;
@@ -114,7 +135,7 @@ __global__ void __launch_bounds__(256) eval_kernel(DevSystem S, const double* __
                         }
                         return r;
                     };
-                    auto SLOT = [&](int j) -> double* { return stg + j * W * 32 + lane; };
+                    auto SLOT = [&](int j) -> double* { return stg + j * W * 32; };  // slot j of this lane: element lane
 
                     // stage 1: common factor, ref kernels.cpp:45-53
                     T f = PW(0);
@@ -124,48 +145,48 @@ __global__ void __launch_bounds__(256) eval_kernel(DevSystem S, const double* __
                     if (k == 1) {
                         T L0 = O::mul(O::one(), f);
                         T val = O::mul(L0, X(0));
-                        O::st_planes(SLOT(0), 32, O::mul(L0, COEF(0)));
+                        st_pr(SLOT(0), lane, 32, O::mul(L0, COEF(0)));
                         valterm = O::mul(val, COEF(1));
                     } else if (k == 2) {
                         const T v0 = X(0), v1 = X(1);
                         T L0 = O::mul(v1, f), L1 = O::mul(v0, f);
                         T val = O::mul(L1, v1);
-                        O::st_planes(SLOT(0), 32, O::mul(L0, COEF(0)));
-                        O::st_planes(SLOT(1), 32, O::mul(L1, COEF(1)));
+                        st_pr(SLOT(0), lane, 32, O::mul(L0, COEF(0)));
+                        st_pr(SLOT(1), lane, 32, O::mul(L1, COEF(1)));
                         valterm = O::mul(val, COEF(2));
                     } else {
                         // forward products L[1] = v0, L[r+2] = L[r+1] * v[r+1]
                         T F = X(0);
-                        O::st_planes(SLOT(1), 32, F);
+                        st_pr(SLOT(1), lane, 32, F);
                         for (int r = 0; r + 2 <= k - 1; ++r) {
                             F = O::mul(F, X(r + 1));
-                            if (r + 2 < k - 1) O::st_planes(SLOT(r + 2), 32, F);
+                            if (r + 2 < k - 1) st_pr(SLOT(r + 2), lane, 32, F);
                         }
                         // F == L[k-1]; backward running product q
                         const T vlast = X(k - 1);
                         T q = vlast;
                         {
-                            T L = O::mul(O::ld_planes(SLOT(k - 2), 32), q);
+                            T L = O::mul(LD(SLOT(k - 2), lane, 32), q);
                             L = O::mul(L, f);
-                            O::st_planes(SLOT(k - 2), 32, O::mul(L, COEF(k - 2)));
+                            st_pr(SLOT(k - 2), lane, 32, O::mul(L, COEF(k - 2)));
                         }
                         for (int r = 1; r <= k - 3; ++r) {
                             q = O::mul(q, X(k - 1 - r));
-                            T L = O::mul(O::ld_planes(SLOT(k - 2 - r), 32), q);
+                            T L = O::mul(LD(SLOT(k - 2 - r), lane, 32), q);
                             L = O::mul(L, f);
-                            O::st_planes(SLOT(k - 2 - r), 32, O::mul(L, COEF(k - 2 - r)));
+                            st_pr(SLOT(k - 2 - r), lane, 32, O::mul(L, COEF(k - 2 - r)));
                         }
                         q = O::mul(q, X(1));
                         {
                             T L = O::mul(q, f);
-                            O::st_planes(SLOT(0), 32, O::mul(L, COEF(0)));
+                            st_pr(SLOT(0), lane, 32, O::mul(L, COEF(0)));
                         }
                         T Lk1 = O::mul(F, f);
                         T val = O::mul(Lk1, vlast);
-                        O::st_planes(SLOT(k - 1), 32, O::mul(Lk1, COEF(k - 1)));
+                        st_pr(SLOT(k - 1), lane, 32, O::mul(Lk1, COEF(k - 1)));
                         valterm = O::mul(val, COEF(k));
                     }
-                    if (ORDER == kRef) O::st_planes(SLOT(k), 32, valterm);
+                    if (ORDER == kRef) st_pr(SLOT(k), lane, 32, valterm);
                 }
                 __syncwarp();
                 // stage 3 (Jacobian): ascending-g ordered gather over the (row, column) map
@@ -173,21 +194,21 @@ __global__ void __launch_bounds__(256) eval_kernel(DevSystem S, const double* __
                 for (int v = lane; v < n; v += 32) {
                     const int li = (p * S.chunks + c) * n + v;
                     const int e0 = __ldg(S.gm_off + li), e1 = __ldg(S.gm_off + li + 1);
-                    T a = c == 0 ? O::zero() : O::ld_planes(acc + v, n + 1);
+                    T a = c == 0 ? O::zero() : LD(acc, v, n + 1);
                     for (int e = e0; e < e1; ++e) {
                         const int ent = __ldg(S.gm_ent + e);
-                        a = O::add(a, O::ld_planes(stg + (ent >> 5) * W * 32 + (ent & 31), 32));
+                        a = O::add(a, LD(stg + (ent >> 5) * W * 32, ent & 31, 32));
                     }
                     if (last)
                         O::st_aos(orow + ((size_t)n + (size_t)p * n + v) * W, a);
                     else
-                        O::st_planes(acc + v, n + 1, a);
+                        st_pr(acc, v, n + 1, a);
                 }
                 // stage 3 (value)
                 if (ORDER == kRef) {
                     if (lane == 0) {
                         const int gl = min(32, m - c * 32);
-                        for (int gg = 0; gg < gl; ++gg) vacc = O::add(vacc, O::ld_planes(stg + k * W * 32 + gg, 32));
+                        for (int gg = 0; gg < gl; ++gg) vacc = O::add(vacc, LD(stg + k * W * 32, gg, 32));
                     }
                 } else {
                     T r = valterm;
