@@ -151,6 +151,7 @@ __constant__ unsigned kRecip[257];
 // n <= 32 (NQ = 1) runs 128-thread CTAs, six per SM (the matrix is 36 KB in dd): 85 registers
 template <int NQ>
 struct NtBounds {
+    // (measured: 160-thread CTAs, four per SM: n = 32 dd -2.7%, complex double +22% time)
     static constexpr int threads = NQ == 1 ? 128 : 256, blocks = NQ == 1 ? PJB_NT_MINB : 1;
 };
 template <class T, int NQ>

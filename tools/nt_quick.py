@@ -13,7 +13,10 @@ tag = os.path.basename(os.environ.get("PJ_LIB_PATH", "default"))
 for (n, m, k, d, B) in [(32, 32, 8, 2, 65536), (64, 64, 16, 10, 8192)]:
     s = pj.random_system(n, m, k, d, 7)
     ctx = pj.EvaluationContext(s)
+    thr = int(os.environ.get("PJ_NT_THREADS", "0"))
     for prec in ["dd", "d"]:
+        if thr:
+            ctx.set_launch(prec, thr, newton=True)
         W = 4 if prec == "dd" else 2
         pts = pj.random_points(n, B, 11)
         p = pj.to_dd(pts) if prec == "dd" else np.stack([pts.real, pts.imag], -1)
