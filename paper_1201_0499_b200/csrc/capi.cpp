@@ -153,6 +153,8 @@ struct pj_ctx {
     // augmented matrix exceeds shared memory, host-API staging buffers
     struct NewtonPlan {
         int blocks = 0, threads = 0, over_threads = 0;
+        int over_variant = 0;  // 0 auto (the column kernel), -1 column kernel, 1 panel (n <= 32)
+        bool panel = false;
         size_t smem = 0;
         bool gscr = false;
     } newton[2];
@@ -360,8 +362,11 @@ int newton_plan(pj_ctx* c, int pi, pj_ctx::NewtonPlan** out) {
         // n <= 32: 128-thread CTAs (the kernel is compiled for at most 128 there, newton.cu)
         P.threads = P.over_threads ? P.over_threads : (c->n <= 32 ? 128 : 256);
         if (c->n <= 32) P.threads = std::min(P.threads, 128);
+        // the panel kernel is opt-in: measured slower at C2 (dd 10.7 vs 7.2 ms, d 2.50 vs 2.44 ms)
+        P.panel = pjb::newton_panel_supported(c->n) && P.over_variant == 1 && mb + ib <= c->smem_optin;
+        if (P.panel) P.threads = std::max(P.threads, 64);  // one look-ahead warp + updaters
         if (mb + ib <= c->smem_optin) {
-            const int nb = pjb::newton_blocks_per_sm(prec, c->n, P.threads, mb + ib);
+            const int nb = pjb::newton_blocks_per_sm(prec, c->n, P.threads, mb + ib, P.panel);
             if (nb > 0) {
                 P.smem = mb + ib;
                 P.blocks = nb * c->sms;
@@ -369,7 +374,8 @@ int newton_plan(pj_ctx* c, int pi, pj_ctx::NewtonPlan** out) {
             }
         }
         if (!P.blocks) {  // augmented matrix beyond shared memory: per-CTA slabs in HBM (L2-resident)
-            const int nb = std::max(1, std::min(pjb::newton_blocks_per_sm(prec, c->n, P.threads, ib), 4));
+            P.panel = false;
+            const int nb = std::max(1, std::min(pjb::newton_blocks_per_sm(prec, c->n, P.threads, ib, false), 4));
             P.smem = ib;
             P.blocks = nb * c->sms;
             P.gscr = true;
@@ -935,6 +941,17 @@ int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points) {
 int pj_set_kernel_variant(pj_ctx* ctx, int flags, int variant) {
     if (!ctx) return fail(PJ_EINVAL, "null context");
     if (ctx->host_only) return fail(PJ_EINVAL, "host-only context");
+    if (flags & PJ_OP_NEWTON) {
+        const int pi = prec_index(flags);
+        if (pi < 0) return fail(PJ_EINVAL, "unknown precision flag");
+        if (variant > 1 || variant < -1) return fail(PJ_EINVAL, "unknown kernel variant");
+        if (variant == 1 && !pjb::newton_panel_supported(ctx->n))
+            return fail(PJ_EINVAL, "newton: the panel kernel needs n <= 32");
+        ctx->newton[pi].over_variant = variant;
+        ctx->newton[pi].blocks = 0;  // re-planned on the next solve
+        g_err.clear();
+        return PJ_OK;
+    }
     const int md = mode_of(flags);
     if (md == kModeDDRef) return fail(PJ_EINVAL, "kernel variants exist for complex double and the fast dd order");
     if (variant > 1 || variant < -1) return fail(PJ_EINVAL, "unknown kernel variant");
@@ -970,7 +987,7 @@ int pj_get_launch(pj_ctx* ctx, int flags, int32_t* threads, int32_t* tile_points
         if (tile_points) *tile_points = 1;
         if (blocks) *blocks = P->blocks;
         if (smem_bytes) *smem_bytes = int64_t(P->smem);
-        if (variant) *variant = P->gscr ? 1 : 0;
+        if (variant) *variant = P->gscr ? 2 : P->panel ? 1 : 0;
         g_err.clear();
         return PJ_OK;
     }
@@ -1019,7 +1036,7 @@ int pj_newton_solve(pj_ctx* ctx, int flags, const double* d_evals, const double*
     a.status = d_status;
     a.gscratch = P->gscr ? ctx->d_nscratch : nullptr;
     a.gstride = (pjb::newton_matrix_bytes(pi + 1, ctx->n) / sizeof(double) + 31) / 32 * 32;
-    cudaError_t e = pjb::launch_newton(pi + 1, a, P->blocks, P->threads, P->smem, (cudaStream_t)stream);
+    cudaError_t e = pjb::launch_newton(pi + 1, a, P->blocks, P->threads, P->smem, P->panel, (cudaStream_t)stream);
     if (prev != ctx->device) cudaSetDevice(prev);
     if (e) return cuda_fail(e, "newton: kernel launch");
     g_err.clear();

@@ -94,7 +94,10 @@ struct NewtonArgs {
 };
 size_t newton_matrix_bytes(int prec, int n);  // matrix planes, inverses, solution
 size_t newton_int_bytes(int n);               // pivot bookkeeping (always in shared memory)
-int newton_blocks_per_sm(int prec, int n, int threads, size_t smem);
-cudaError_t launch_newton(int prec, const NewtonArgs& args, int blocks, int threads, size_t smem, cudaStream_t st);
+// panel = the blocked kernel for n <= 32 (newton_panel_kernel), else the column kernel
+bool newton_panel_supported(int n);
+int newton_blocks_per_sm(int prec, int n, int threads, size_t smem, bool panel);
+cudaError_t launch_newton(int prec, const NewtonArgs& args, int blocks, int threads, size_t smem, bool panel,
+                          cudaStream_t st);
 
 }  // namespace pjb

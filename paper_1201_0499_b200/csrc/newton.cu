@@ -141,6 +141,108 @@ __device__ __forceinline__ CDD shfl_idx<CDD>(CDD v, int src) {
             __shfl_sync(0xffffffffu, v.ih, src), __shfl_sync(0xffffffffu, v.il, src)};
 }
 
+// ---- pieces shared by the two Newton kernels
+// Load [J | y − f] of point b (all threads; warp 0 the right-hand side, its norm, the identity row
+// list). Shared-memory matrices: 8-byte cp.async copies straight into the pair layout (no
+// registers, every copy in flight at once); global slabs: plain loads. The caller waits + syncs.
+template <class T>
+__device__ __forceinline__ void nt_load(const NewtonArgs& a, long long b, double* A, int* list, int* sing) {
+    using S = Sc<T>;
+    constexpr int W = S::W;
+    const int n = a.n, ld = n + 1, P = n * ld;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const double* ev = a.evals + size_t(b) * (size_t(n) * n + n) * W;
+    if (!a.gscratch) {
+        for (int t = tid; t < n * n * W; t += nt) {
+            const int el = t / W, comp = t - el * W;
+            const int i = el / n, j = el - i * n;
+            const unsigned dst = unsigned(__cvta_generic_to_shared(A + NL<T>::off(i * ld + j, comp, P)));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(ev + size_t(n) * W + t));
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    } else {
+        for (int t = tid; t < n * n; t += nt) {
+            const int i = t / n, j = t - i * n;
+            NL<T>::st(A, i * ld + j, P, S::ld_aos(ev + size_t(n + t) * W));
+        }
+    }
+    if (warp == 0) {
+        double rn = 0.0;
+        for (int i = lane; i < n; i += 32) {
+            T r = nt_neg(S::ld_aos(ev + size_t(i) * W));
+            if (a.target) r = S::add(S::ld_aos(a.target + (size_t(b) * n + i) * W), r);
+            NL<T>::st(A, i * ld + n, P, r);
+            rn = fmax(rn, nt_magmax(r));
+            list[i] = i;
+        }
+        for (int o = 16; o; o >>= 1) rn = fmax(rn, __shfl_xor_sync(0xffffffffu, rn, o));
+        if (lane == 0) {
+            if (a.norms) a.norms[2 * b] = rn;
+            *sing = 0;
+        }
+    }
+}
+
+// Back substitution (warp 0): rhs of physical rows lane + 32q in registers;
+// dx_s = rhs[piv_s] * inv_s, then rhs[piv_t] -= A[piv_t][s] * dx_s for t < s; x_new = x + dx.
+template <class T, int NQ>
+__device__ __forceinline__ void nt_back_substitute(const NewtonArgs& a, long long b, const double* A,
+                                                   const double* INV, double* DX, const int* s_piv,
+                                                   const int* s_step, bool singular) {
+    using S = Sc<T>;
+    constexpr int W = S::W;
+    const int n = a.n, ld = n + 1, P = n * ld, lane = threadIdx.x & 31;
+    const double* x = a.points + size_t(b) * n * W;
+    double* xo = a.points_out + size_t(b) * n * W;
+    if (singular) {
+        for (int i = lane; i < n; i += 32) S::st_aos(xo + size_t(i) * W, S::ld_aos(x + size_t(i) * W));
+        if (lane == 0) {
+            if (a.norms) a.norms[2 * b + 1] = INFINITY;
+            if (a.status) a.status[b] = 1;
+        }
+        return;
+    }
+    T rr[NQ];
+    int st[NQ];
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+        const int r = lane + 32 * q;
+        rr[q] = r < n ? NL<T>::ld(A, r * ld + n, P) : S::zero();
+        st[q] = r < n ? s_step[r] : -1;
+    }
+    for (int s = n - 1; s >= 0; --s) {
+        const int pr = s_piv[s];
+        const int owner = pr & 31, qi = pr >> 5;
+        T xs = rr[0];
+#pragma unroll
+        for (int q = 1; q < NQ; ++q)
+            if (q == qi) xs = rr[q];
+        xs = shfl_idx(xs, owner);
+        xs = S::mul(xs, NL<T>::ld(INV, s, n));
+        if (lane == 0) NL<T>::st(DX, s, n, xs);
+#pragma unroll
+        for (int q = 0; q < NQ; ++q)
+            if (st[q] >= 0 && st[q] < s)
+                rr[q] = S::add(rr[q], nt_neg(nt_umul(NL<T>::ld(A, (lane + 32 * q) * ld + s, P), xs)));
+    }
+    __syncwarp();
+    double dn = 0.0;
+    bool fin = true;
+    for (int i = lane; i < n; i += 32) {
+        const T d = NL<T>::ld(DX, i, n);
+        const T xn = S::add(S::ld_aos(x + size_t(i) * W), d);
+        S::st_aos(xo + size_t(i) * W, xn);
+        dn = fmax(dn, nt_magmax(d));
+        fin = fin && nt_finite(xn);
+    }
+    for (int o = 16; o; o >>= 1) dn = fmax(dn, __shfl_xor_sync(0xffffffffu, dn, o));
+    fin = __all_sync(0xffffffffu, fin);
+    if (lane == 0) {
+        if (a.norms) a.norms[2 * b + 1] = dn;
+        if (a.status) a.status[b] = fin ? 0 : 2;
+    }
+}
+
 // NQ: active-row slots per lane (look-ahead) and rows per lane (back substitution), n <= 32*NQ
 // kRecip[c] = ceil(2^16 / c): floor(x / c) == (x * kRecip[c]) >> 16 for x, c <= 256
 __constant__ unsigned kRecip[257];
@@ -154,8 +256,14 @@ struct NtBounds {
     // (measured: 160-thread CTAs, four per SM: n = 32 dd -2.7%, complex double +22% time)
     static constexpr int threads = NQ == 1 ? 128 : 256, blocks = NQ == 1 ? PJB_NT_MINB : 1;
 };
+#ifndef PJB_NT_MINB_D
+#define PJB_NT_MINB_D 7
+#endif
+// complex double at n <= 32 (18 KB of matrix): more CTAs per SM fit, a tighter register budget
 template <class T, int NQ>
-__global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) newton_kernel(NewtonArgs a) {
+constexpr int nt_min_blocks() { return NQ == 1 && Sc<T>::W == 2 ? PJB_NT_MINB_D : NtBounds<NQ>::blocks; }
+template <class T, int NQ>
+__global__ void __launch_bounds__(NtBounds<NQ>::threads, nt_min_blocks<T, NQ>()) newton_kernel(NewtonArgs a) {
     using S = Sc<T>;
     constexpr int W = S::W;
     extern __shared__ __align__(16) double smem[];
@@ -171,7 +279,6 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
     double* A = a.gscratch ? a.gscratch + size_t(blockIdx.x) * a.gstride : smem + newton_int_words(n);
     double* INV = A + size_t(W) * P;  // [W][n] pivot inverses
     double* DX = INV + size_t(W) * n;   // [W][n] solution
-    const size_t nout = size_t(n) * n + n;
 
 #ifdef PJB_NT_TRACE
     long long* tsub = nullptr;  // look-ahead sub-phase clocks (developer instrumentation)
@@ -243,38 +350,7 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
         PJB_TSUB(c, 3)
     };
     for (long long b = blockIdx.x; b < a.B; b += gridDim.x) {
-        const double* ev = a.evals + size_t(b) * nout * W;
-        // ---- load [J | y − f]. Shared-memory matrices: 8-byte cp.async copies straight into the
-        // pair layout (no registers, every copy in flight at once); global slabs: plain loads
-        if (!a.gscratch) {
-            for (int t = tid; t < n * n * W; t += nt) {
-                const int el = t / W, comp = t - el * W;
-                const int i = el / n, j = el - i * n;
-                const unsigned dst = unsigned(__cvta_generic_to_shared(A + NL<T>::off(i * ld + j, comp, P)));
-                asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(ev + size_t(n) * W + t));
-            }
-            asm volatile("cp.async.commit_group;\n" ::);
-        } else {
-            for (int t = tid; t < n * n; t += nt) {
-                const int i = t / n, j = t - i * n;
-                NL<T>::st(A, i * ld + j, P, S::ld_aos(ev + size_t(n + t) * W));
-            }
-        }
-        if (warp == 0) {
-            double rn = 0.0;
-            for (int i = lane; i < n; i += 32) {
-                T r = nt_neg(S::ld_aos(ev + size_t(i) * W));
-                if (a.target) r = S::add(S::ld_aos(a.target + (size_t(b) * n + i) * W), r);
-                NL<T>::st(A, i * ld + n, P, r);
-                rn = fmax(rn, nt_magmax(r));
-                s_list0[i] = i;
-            }
-            for (int o = 16; o; o >>= 1) rn = fmax(rn, __shfl_xor_sync(0xffffffffu, rn, o));
-            if (lane == 0) {
-                if (a.norms) a.norms[2 * b] = rn;
-                s_sing = 0;
-            }
-        }
+        nt_load<T>(a, b, A, s_list0, &s_sing);
         asm volatile("cp.async.wait_all;\n" ::);
         __syncthreads();
         // ---- column 0: pivot, inverse, multipliers
@@ -384,59 +460,197 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, NtBounds<NQ>::blocks) n
             singular = s_sing != 0;
         }
 
-        // ---- back substitution (warp 0): rhs of physical rows lane + 32q in registers;
-        // dx_s = rhs[piv_s] * inv_s, then rhs[piv_t] -= A[piv_t][s] * dx_s for t < s
-        if (warp == 0) {
-            const double* x = a.points + size_t(b) * n * W;
-            double* xo = a.points_out + size_t(b) * n * W;
-            if (singular) {
-                for (int i = lane; i < n; i += 32) S::st_aos(xo + size_t(i) * W, S::ld_aos(x + size_t(i) * W));
-                if (lane == 0) {
-                    if (a.norms) a.norms[2 * b + 1] = INFINITY;
-                    if (a.status) a.status[b] = 1;
-                }
-            } else {
-                T rr[NQ];
-                int st[NQ];
+        if (warp == 0) nt_back_substitute<T, NQ>(a, b, A, INV, DX, s_piv, s_step, singular);
+        __syncthreads();  // the next point reuses the matrix storage
+    }
+}
+
+// ---- blocked variant for n <= 32 (opt-in, pj_set_kernel_variant with PJ_OP_NEWTON): the
+// look-ahead warp factors PANELS of kPW columns in registers (lane = row), the other warps apply a
+// panel's kPW steps to the trailing columns in one pass. Measured slower than the column kernel at
+// C2 (dd 10.7 vs 7.2 ms, complex double 2.50 vs 2.44 ms): the look-ahead's 32 sequential pivot
+// chains are the critical path either way, and the panel look-ahead adds the next panel's update
+// to it (and, in dd, register pressure).
+// The arithmetic of every element is the unblocked kernel's (same pivots, multipliers, and per
+// element the same update sequence in step order), so results are bit-identical; what changes is
+// the schedule: one CTA barrier per panel instead of per column, the look-ahead's column values
+// and multipliers stay in registers, and a trailing element loads once for kPW updates.
+constexpr int kPW = 4;
+
+#ifndef PJB_NTP_MINB
+#define PJB_NTP_MINB 3
+#endif
+template <class T>
+__global__ void __launch_bounds__(128, PJB_NTP_MINB) newton_panel_kernel(NewtonArgs a) {
+    using S = Sc<T>;
+    constexpr int W = S::W;
+    extern __shared__ __align__(16) double smem[];
+    __shared__ int s_sing;
+    const int n = a.n, ld = n + 1, P = n * ld;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    int* s_piv = reinterpret_cast<int*>(smem);
+    int* s_step = s_piv + n;
+    int* s_list[2] = {s_step + n, s_step + 2 * n};  // rows active at a panel's start (compacted)
+    double* A = smem + newton_int_words(n);
+    double* INV = A + size_t(W) * P;
+    double* DX = INV + size_t(W) * n;
+    const int NP = (n + kPW - 1) / kPW;
+    const bool valid = lane < n;  // warp 0: lane = row
+
+    for (long long b = blockIdx.x; b < a.B; b += gridDim.x) {
+        nt_load<T>(a, b, A, s_list[0], &s_sing);
+        if (warp == 0)
+            for (int i = lane; i < n; i += 32) s_step[i] = n;  // n = not yet pivoted
+        asm volatile("cp.async.wait_all;\n" ::);
+        __syncthreads();
+
+        // look-ahead state (warp 0): my row's values in the current panel's columns, its
+        // multipliers for those columns, the step it was pivoted at
+        T V[kPW], Lm[kPW];
+        int mystep = n;
+        bool bad = false;
+        // factor panel p from V (columns c0..c0+w-1 updated through step c0-1): pivots, inverses,
+        // multipliers (registers + shared memory for the trailing update), the pivot rows' panel
+        // entries (U), and the compacted list of rows active at the panel's start
+        auto factor = [&](int p) {
+            const int c0 = p * kPW, w = min(kPW, n - c0);
+            const unsigned act = __ballot_sync(0xffffffffu, valid && mystep == n);
+            if (valid && mystep == n) s_list[p & 1][__popc(act & ((1u << lane) - 1))] = lane;
 #pragma unroll
-                for (int q = 0; q < NQ; ++q) {
-                    const int r = lane + 32 * q;
-                    rr[q] = r < n ? NL<T>::ld(A, r * ld + n, P) : S::zero();
-                    st[q] = r < n ? s_step[r] : -1;
-                }
-                for (int s = n - 1; s >= 0; --s) {
-                    const int pr = s_piv[s];
-                    const int owner = pr & 31, qi = pr >> 5;
-                    T xs = rr[0];
+            for (int t = 0; t < kPW; ++t) {
+                if (t < w && !bad) {
+                    const int col = c0 + t;
+                    const bool active = valid && mystep == n;
+                    const T v = V[t];
+                    const T ivq = nt_inv(v);  // speculative: off the arg-max's path
+                    const double mg = active ? nt_mag1(v) : 0.0;
+                    const unsigned long long bits = __double_as_longlong(mg);
+                    const unsigned hi = unsigned(bits >> 32), lo = unsigned(bits);
+                    const unsigned mh = __reduce_max_sync(0xffffffffu, hi);
+                    const unsigned ml = __reduce_max_sync(0xffffffffu, hi == mh ? lo : 0u);
+                    const bool cand = active && mg > 0.0 && hi == mh && lo == ml;
+                    const unsigned cm = __ballot_sync(0xffffffffu, cand);
+                    if (!cm) {  // no nonzero pivot: singular
+                        if (lane == 0) s_sing = 1;
+                        bad = true;
+                    } else {
+                        const int pr = __ffs(cm) - 1;  // ties: the smallest row
+                        const T iv = shfl_idx(ivq, pr);
+                        if (lane == pr) {
+                            mystep = col;
+                            s_piv[col] = pr;
+                            s_step[pr] = col;
+                            NL<T>::st(INV, col, n, iv);
+                        }
+                        const bool upd = active && lane != pr;
+                        T l = S::zero();
+                        if (upd) {
+                            l = S::mul(v, iv);
+                            NL<T>::st(A, lane * ld + col, P, l);
+                        }
+                        Lm[t] = l;
 #pragma unroll
-                    for (int q = 1; q < NQ; ++q)
-                        if (q == qi) xs = rr[q];
-                    xs = shfl_idx(xs, owner);
-                    xs = S::mul(xs, NL<T>::ld(INV, s, n));
-                    if (lane == 0) NL<T>::st(DX, s, n, xs);
-#pragma unroll
-                    for (int q = 0; q < NQ; ++q)
-                        if (st[q] >= 0 && st[q] < s)
-                            rr[q] = S::add(rr[q], nt_neg(nt_umul(NL<T>::ld(A, (lane + 32 * q) * ld + s, P), xs)));
-                }
-                __syncwarp();
-                double dn = 0.0;
-                bool fin = true;
-                for (int i = lane; i < n; i += 32) {
-                    const T d = NL<T>::ld(DX, i, n);
-                    const T xn = S::add(S::ld_aos(x + size_t(i) * W), d);
-                    S::st_aos(xo + size_t(i) * W, xn);
-                    dn = fmax(dn, nt_magmax(d));
-                    fin = fin && nt_finite(xn);
-                }
-                for (int o = 16; o; o >>= 1) dn = fmax(dn, __shfl_xor_sync(0xffffffffu, dn, o));
-                fin = __all_sync(0xffffffffu, fin);
-                if (lane == 0) {
-                    if (a.norms) a.norms[2 * b + 1] = dn;
-                    if (a.status) a.status[b] = fin ? 0 : 2;
+                        for (int t2 = t + 1; t2 < kPW; ++t2) {
+                            if (t2 < w) {
+                                const T u = shfl_idx(V[t2], pr);
+                                if (upd) V[t2] = S::add(V[t2], nt_neg(nt_umul(l, u)));
+                                if (lane == pr) NL<T>::st(A, lane * ld + c0 + t2, P, V[t2]);  // U entry
+                            }
+                        }
+                    }
                 }
             }
+        };
+        if (warp == 0) {
+#pragma unroll
+            for (int t = 0; t < kPW; ++t) V[t] = valid && t < n ? NL<T>::ld(A, lane * ld + t, P) : S::zero();
+            factor(0);
         }
+        __syncthreads();
+        bool singular = s_sing != 0;
+        for (int p = 0; p < NP && !singular; ++p) {
+            const int c0 = p * kPW, w = min(kPW, n - c0);
+            const int c1 = c0 + kPW, w1 = c1 < n ? min(kPW, n - c1) : 0;
+            if (warp == 0) {
+                if (w1 > 0) {
+                    // next panel's columns (current through step c0-1), then panel p's steps in order
+                    T* V2 = V;  // panel p's values are dead once factored: reuse their registers
+#pragma unroll
+                    for (int t = 0; t < kPW; ++t)
+                        V2[t] = valid && t < w1 ? NL<T>::ld(A, lane * ld + c1 + t, P) : S::zero();
+#pragma unroll
+                    for (int t = 0; t < kPW; ++t) {
+                        if (t < w) {
+                            const int pr = s_piv[c0 + t];
+                            const bool upd = valid && mystep > c0 + t;
+#pragma unroll
+                            for (int t2 = 0; t2 < kPW; ++t2) {
+                                const T u = shfl_idx(V2[t2], pr);
+                                if (upd && t2 < w1) V2[t2] = S::add(V2[t2], nt_neg(nt_umul(Lm[t], u)));
+                            }
+                        }
+                    }
+                    // rows pivoted in panel p: their entries of the next panel are final (U)
+                    if (valid && mystep >= c0 && mystep < c0 + w)
+#pragma unroll
+                        for (int t = 0; t < kPW; ++t)
+                            if (t < w1) NL<T>::st(A, lane * ld + c1 + t, P, V2[t]);
+                    factor(p + 1);
+                }
+            } else {
+                // trailing columns beyond the next panel (rhs included) with panel p's steps. Phase A:
+                // each thread forms the pivot rows' entries of its column after the panel's earlier
+                // steps (u_t); named barrier; phase B: every row active at the panel's start gets
+                // its updates in step order (pivot rows of the panel: the updates before their step).
+                const int j0 = w1 > 0 ? c1 + w1 : c0 + w, Cp = n + 1 - j0, Tp = nt - 32, tp = tid - 32;
+                const int* list = s_list[p & 1];
+                const int R0 = n - c0;
+                // panel p's pivot rows (written before the last barrier; s_step may be changing under
+                // the look-ahead's factor(p + 1), so row activity is read from these instead)
+                int pvt[kPW];
+#pragma unroll
+                for (int t = 0; t < kPW; ++t) pvt[t] = t < w ? s_piv[c0 + t] : -1;
+                for (int cb = 0; cb < Cp; cb += Tp) {  // uniform pass count: every updater joins each barrier
+                    const int cw = min(Tp, Cp - cb);
+                    const unsigned rc = kRecip[cw];
+                    const int G = int((unsigned(Tp) * rc) >> 16), rg = int((unsigned(tp) * rc) >> 16);
+                    const bool mine = rg < G;
+                    const int j = j0 + cb + (tp - rg * cw);
+                    T u[kPW];
+                    if (mine) {
+#pragma unroll
+                        for (int t = 0; t < kPW; ++t) {
+                            if (t < w) {
+                                const int pr = pvt[t];
+                                T x = NL<T>::ld(A, pr * ld + j, P);
+#pragma unroll
+                                for (int t2 = 0; t2 < kPW; ++t2)
+                                    if (t2 < t) x = S::add(x, nt_neg(nt_umul(NL<T>::ld(A, pr * ld + c0 + t2, P), u[t2])));
+                                u[t] = x;
+                            }
+                        }
+                    }
+                    asm volatile("bar.sync 1, %0;\n" ::"r"(Tp));
+                    if (mine) {
+                        for (int idx = rg; idx < R0; idx += G) {
+                            const int r = list[idx];
+                            int sr = n;  // the step row r is pivoted at, if within panel p
+#pragma unroll
+                            for (int t = 0; t < kPW; ++t)
+                                if (r == pvt[t]) sr = c0 + t;
+                            T x = NL<T>::ld(A, r * ld + j, P);
+#pragma unroll
+                            for (int t = 0; t < kPW; ++t)
+                                if (t < w && sr > c0 + t) x = S::add(x, nt_neg(nt_umul(NL<T>::ld(A, r * ld + c0 + t, P), u[t])));
+                            NL<T>::st(A, r * ld + j, P, x);
+                        }
+                    }
+                }
+            }
+            __syncthreads();
+            singular = s_sing != 0;
+        }
+        if (warp == 0) nt_back_substitute<T, 1>(a, b, A, INV, DX, s_piv, s_step, singular);
         __syncthreads();  // the next point reuses the matrix storage
     }
 }
@@ -451,7 +665,10 @@ const void* newton_fn(int nq) {
     }
 }
 int nq_of(int n) { return n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : 8; }
-const void* fn_of(int prec, int n) { return prec == 1 ? newton_fn<CD>(nq_of(n)) : newton_fn<CDD>(nq_of(n)); }
+const void* fn_of(int prec, int n, bool panel) {
+    if (panel) return prec == 1 ? (const void*)newton_panel_kernel<CD> : (const void*)newton_panel_kernel<CDD>;
+    return prec == 1 ? newton_fn<CD>(nq_of(n)) : newton_fn<CDD>(nq_of(n));
+}
 
 }  // namespace
 
@@ -478,17 +695,20 @@ static cudaError_t init_recip() {
     return e;
 }
 
-int newton_blocks_per_sm(int prec, int n, int threads, size_t smem) {
-    const void* f = fn_of(prec, n);
+bool newton_panel_supported(int n) { return n <= 32; }
+
+int newton_blocks_per_sm(int prec, int n, int threads, size_t smem, bool panel) {
+    const void* f = fn_of(prec, n, panel);
     if (smem) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, threads, smem) != cudaSuccess) return 0;
     return nb;
 }
 
-cudaError_t launch_newton(int prec, const NewtonArgs& args, int blocks, int threads, size_t smem, cudaStream_t st) {
+cudaError_t launch_newton(int prec, const NewtonArgs& args, int blocks, int threads, size_t smem, bool panel,
+                          cudaStream_t st) {
     if (args.B <= 0) return cudaSuccess;
-    const void* f = fn_of(prec, args.n);
+    const void* f = fn_of(prec, args.n, panel && !args.gscratch);
     if (cudaError_t e = init_recip()) return e;
     if (smem) {
         cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));

@@ -512,10 +512,12 @@ class EvaluationContext:
         f = _flags(precision, order) | (_lib.PJ_OP_NEWTON if newton else 0)
         check(lib().pj_set_launch(self._h, f, threads, tile_points))
 
-    def set_variant(self, variant: int, precision: str = "dd") -> None:
+    def set_variant(self, variant: int, precision: str = "dd", newton: bool = False) -> None:
         """Kernel choice (pj_set_kernel_variant) for complex double ("d") or the fast dd order:
-        0 auto, -1 generic, 1 k-specialised."""
-        check(lib().pj_set_kernel_variant(self._h, _flags(precision, None), variant))
+        0 auto, -1 generic, 1 k-specialised; newton=True: the Newton solve (-1 column kernel,
+        1 panel kernel for n <= 32)."""
+        f = _flags(precision, None) | (_lib.PJ_OP_NEWTON if newton else 0)
+        check(lib().pj_set_kernel_variant(self._h, f, variant))
 
     def launch(self, precision: str, order: str | None = None, newton: bool = False):
         t, tp, b, var = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()

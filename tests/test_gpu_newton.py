@@ -186,3 +186,22 @@ def test_step_device_chunked_fork_join(gpu):
     want, _, wst = O.newton_solve("dd", 32, O.evaluate("dd", S, p, threads=8), p, threads=8)
     assert np.array_equal(x2.cpu().numpy().view(np.uint64), want.view(np.uint64))
     assert np.array_equal(st.cpu().numpy(), wst)
+
+
+@pytest.mark.parametrize("prec", ["d", "dd"])
+def test_panel_kernel_bit_identical(prec, gpu):
+    # the opt-in blocked solve (n <= 32) computes the same bits as the column kernel and the oracle
+    for (n, m, k, d, B) in [(32, 32, 8, 2, 70), (30, 12, 5, 3, 9), (13, 4, 3, 4, 11), (5, 3, 2, 2, 4)]:
+        s, S, pts = shaped(n, m, k, d, B)
+        ctx = pj.EvaluationContext(s)
+        ctx.set_variant(1, prec, newton=True)
+        assert ctx.launch(prec, newton=True)["variant"] == 1
+        p = np.stack([pts.real, pts.imag], -1) if prec == "d" else pj.to_dd(pts)
+        ev = O.evaluate(prec, S, p)
+        tg = 0.25 * np.roll(ev[:, :n], 1, axis=0)
+        want = O.newton_solve(prec, n, ev, p, target=tg)
+        got = solve_gpu(ctx, prec, ev, p, target=tg)
+        assert np.array_equal(got[2], want[2])
+        assert np.array_equal(got[0].view(np.uint64), want[0].view(np.uint64))
+    with pytest.raises(ValueError):
+        pj.EvaluationContext(pj.random_system(40, 4, 3, 2, 1)).set_variant(1, "dd", newton=True)
