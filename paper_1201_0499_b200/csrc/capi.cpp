@@ -41,6 +41,26 @@ int cuda_fail(cudaError_t e, const char* what) {
         if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
     } while (0)
 
+// Switches to a context's device for the duration of a call and restores the caller's device on
+// every exit path (early error returns included).
+struct DeviceGuard {
+    int prev = -1;
+    bool switched = false;
+    cudaError_t enter(int dev) {
+        cudaError_t e = cudaGetDevice(&prev);
+        if (e) return e;
+        if (prev != dev) {
+            e = cudaSetDevice(dev);
+            if (e) return e;
+            switched = true;
+        }
+        return cudaSuccess;
+    }
+    ~DeviceGuard() {
+        if (switched) cudaSetDevice(prev);
+    }
+};
+
 // ------------------------------------------------------------------ validation
 // Rules and wording follow validate_system, ref src/system.cpp:21-64 (violations as data);
 // the byte-encoding cap n <= 256 follows build_layout, ref src/packing.cpp:25-27.
@@ -719,9 +739,8 @@ int pj_evaluate_host(pj_ctx* ctx, int flags, const double* h_points, int64_t bat
     chunk = std::min<int64_t>(chunk, batch);
     const int nchunks = int((batch + chunk - 1) / chunk);
     const int ns = std::min(nchunks, int(pj_ctx::kHostStreams));
-    int prev = 0;
-    cudaGetDevice(&prev);
-    PJ_CUDA(cudaSetDevice(ctx->device));
+    DeviceGuard dg;
+    PJ_CUDA(dg.enter(ctx->device));
     if (size_t(chunk) * in_pt > ctx->in_cap || size_t(chunk) * out_pt > ctx->out_cap) {
         for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
             cudaFree(ctx->d_in[i]);
@@ -752,13 +771,9 @@ int pj_evaluate_host(pj_ctx* ctx, int flags, const double* h_points, int64_t bat
         cudaError_t e = cudaStreamSynchronize(ctx->hstream[i]);
         if (e && rc == PJ_OK) rc = cuda_fail(e, "evaluate_host: stream");
     }
-    if (rc) {
-        cudaSetDevice(prev);
-        return rc;
-    }
+    if (rc) return rc;
     int seen = 0;
     rc = pj_nonfinite_seen(ctx, ctx->hstream[0], &seen);
-    cudaSetDevice(prev);
     if (rc) return rc;
     if (seen) return fail(PJ_ENONFINITE, "evaluate: non-finite coordinate");
     g_err.clear();
@@ -1130,9 +1145,8 @@ int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double*
     chunk = std::min<int64_t>(chunk, batch);
     const int nchunks = int((batch + chunk - 1) / chunk);
     const int ns = std::min(nchunks, int(pj_ctx::kHostStreams));
-    int prev = 0;
-    cudaGetDevice(&prev);
-    PJ_CUDA(cudaSetDevice(ctx->device));
+    DeviceGuard dg;
+    PJ_CUDA(dg.enter(ctx->device));
     if (size_t(chunk) * x_pt > ctx->nx_cap || size_t(chunk) * out_pt > ctx->nwork_cap) {
         for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
             cudaFree(ctx->d_nx[i]);
@@ -1183,13 +1197,9 @@ int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double*
         if (e && rc == PJ_OK) rc = cuda_fail(e, "newton_host: stream");
     }
     cudaStream_t st = ctx->hstream[0];
-    if (rc) {
-        cudaSetDevice(prev);
-        return rc;
-    }
+    if (rc) return rc;
     int seen = 0;
     rc = pj_nonfinite_seen(ctx, st, &seen);
-    cudaSetDevice(prev);
     if (rc) return rc;
     if (seen) return fail(PJ_ENONFINITE, "evaluate: non-finite coordinate");
     g_err.clear();
