@@ -36,3 +36,22 @@ def test_newton_model_flops():
     # n = 32: 11,968 complex products and 11,440 complex additions per solve (docstring of the model)
     assert bench.newton_model_flops(32) == 11968 * 80 + 11440 * 40
     assert bench.newton_model_flops(1) == 2 * 80 + 1 * 40  # one inverse, one dx product, x + dx
+
+
+@pytest.mark.gpu
+def test_bench_json_line_on_gpu(gpu):
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3",
+                        "--e2e-steps", "1", "--ref-seconds", "0.5"], capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "roofline", "e2e", "gpu_launches", "clocks",
+                "cpu_baseline", "quality_up", "c3", "newton"):
+        assert key in line, key
+    assert line["steps"] == 3 and line["warmup"] == 3 and line["n_gpus"] == 1 and line["value"] > 1e6
+    roof = line["roofline"]
+    assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(roof) and roof["frac"] > 0.5
+    assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
+    assert line["gpu_launches"] == 3 and line["cpu_baseline"]["kind"] == "reference"
+    assert line["parity_gate"]["max_err_over_sum_abs_terms"] <= line["parity_gate"]["tol"]
+    assert line["newton"]["status_ok_frac"] == 1.0
