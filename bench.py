@@ -224,6 +224,8 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=4.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--order", default="fast", choices=["fast", "ref"])
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for the barrier and the max-over-ranks timing reduction")
     ap.add_argument("--no-extras", action="store_true",
                     help="skip the secondary lines (C3, C4 quality-up factor, f1 Newton step)")
     args = ap.parse_args()
@@ -236,11 +238,22 @@ def main():
 
     ws, rank, local = dist_env()
     dist = ws > 1
+    # one rank per GPU; --dist-backend gloo lets several ranks share a device (multi-rank checks of
+    # this harness on a one-GPU box: tests/test_bench_contract.py)
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if dist:
         import torch.distributed as tdist
-        tdist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            tdist.init_process_group("nccl", device_id=dev)
+        else:
+            tdist.init_process_group("gloo")
+
+    def max_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device=dev if args.dist_backend == "nccl" else "cpu")
+        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
+        return float(t.item())
 
     def barrier():
         if dist:
@@ -294,9 +307,7 @@ def main():
     per = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
     total_ms = evs[0].elapsed_time(evs[-1])
     if dist:
-        t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        total_ms = float(t.item())
+        total_ms = max_over_ranks(total_ms)
     value = B * ws * args.steps / (total_ms * 1e-3)
     ms_per_step = total_ms / args.steps
     kern_ms = statistics.mean(per)
@@ -313,9 +324,7 @@ def main():
         ctx.evaluate_host(ni, "dd", args.order, out=no)
     e2e_s = time.perf_counter() - t0
     if dist:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        tdist.all_reduce(t, op=tdist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+        e2e_s = max_over_ranks(e2e_s)
     e2e = {"value": Be * ws * args.e2e_steps / e2e_s, "unit": "evals/s", "h2d_bytes_per_step": int(ni.nbytes),
            "d2h_bytes_per_step": int(no.nbytes), "steps": args.e2e_steps,
            "api": "EvaluationContext.evaluate_host -> pj_evaluate_host (3-stream chunked H2D/kernel/D2H)"}

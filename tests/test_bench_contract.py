@@ -55,3 +55,19 @@ def test_bench_json_line_on_gpu(gpu):
     assert line["gpu_launches"] == 3 and line["cpu_baseline"]["kind"] == "reference"
     assert line["parity_gate"]["max_err_over_sum_abs_terms"] <= line["parity_gate"]["tol"]
     assert line["newton"]["status_ok_frac"] == 1.0
+
+
+@pytest.mark.gpu
+def test_bench_two_ranks_on_one_gpu(gpu):
+    # the multi-rank path of the harness (shards, barrier, max-over-ranks timing, rank-0 line) with
+    # two ranks sharing the box's GPU over gloo; the driver's N-GPU runs use one GPU per rank + NCCL
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"), "--gpus", "2",
+           "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--no-extras", "--dist-backend", "gloo"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")]
+    assert len(lines) == 1  # rank 0 alone prints
+    line = json.loads(lines[0])
+    assert line["n_gpus"] == 2 and line["config"]["global_points"] == 2 * 65536 and line["scaling"] == "weak"
+    assert line["value"] > 1e6 and "cpu_baseline" not in line  # the CPU baseline is N=1 only
