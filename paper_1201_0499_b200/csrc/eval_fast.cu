@@ -32,10 +32,6 @@ namespace pjb {
 
 namespace {
 
-__device__ __forceinline__ CDD shfl_cdd(const CDD& v, int src) {
-    return {__shfl_sync(0xffffffffu, v.rh, src), __shfl_sync(0xffffffffu, v.rl, src),
-            __shfl_sync(0xffffffffu, v.ih, src), __shfl_sync(0xffffffffu, v.il, src)};
-}
 __device__ __forceinline__ CDD sel_cdd(bool c, const CDD& a, const CDD& b) {
     return {c ? a.rh : b.rh, c ? a.rl : b.rl, c ? a.ih : b.ih, c ? a.il : b.il};
 }
@@ -48,9 +44,6 @@ __device__ __forceinline__ CDD ld_hl(const double* p, int hl) {
 __device__ __forceinline__ void st_hl(double* p, int hl, const CDD& v) {
     *reinterpret_cast<double2*>(p) = make_double2(v.rh, v.ih);
     *reinterpret_cast<double2*>(p + hl) = make_double2(v.rl, v.il);
-}
-__device__ __forceinline__ CDD ldg_coef(const double* q, int nm) {
-    return {__ldg(q), __ldg(q + nm), __ldg(q + 2 * nm), __ldg(q + 3 * nm)};
 }
 __device__ __forceinline__ CDD ld_aos(const double* p) {
     double2 a = reinterpret_cast<const double2*>(p)[0];
