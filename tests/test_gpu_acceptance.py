@@ -82,3 +82,31 @@ def test_criterion6_determinism(gpu):
     # a batch evaluates each point exactly as a batch of one would
     one = np.concatenate([ctx.evaluate_dd(p4[b:b + 1]) for b in range(0, 301, 50)])
     assert np.array_equal(one.view(np.uint64), base[::50].view(np.uint64))
+
+
+def test_fuzz_reference_order_and_newton(gpu):
+    # 120 random shapes: dd reference order bit-equal to the oracle's restatement, the dd fast order
+    # within the contract, and a Newton step bit-exact with the oracle in both precisions
+    rng = np.random.default_rng(77)
+    for i in range(120):
+        n = int(rng.integers(1, 41))
+        m = int(rng.integers(1, 70))
+        k = int(rng.integers(1, min(n, 24) + 1))
+        d = int(rng.choice([1, 2, 3, 5, 12]))
+        B = int(rng.integers(1, 6))
+        s = pj.random_system(n, m, k, d, 30_000 + i)
+        S = sysd_of(s)
+        ctx = pj.EvaluationContext(s)
+        z = pj.random_points(n, B, 40_000 + i)
+        p4 = pj.to_dd(z)
+        p4[..., 1] = p4[..., 0] * 2.0 ** -53 * rng.uniform(-1, 1, p4[..., 0].shape)
+        want, ms = O.evaluate("dd", S, p4, magsum=True)
+        assert np.array_equal(ctx.evaluate_dd(p4, order="ref"), want), (n, m, k, d)
+        assert dd_rel(ctx.evaluate_dd(p4), want, ms) <= DD_TOL, (n, m, k, d)
+        x, _, st = ctx.newton_host(p4, "dd", order="ref")
+        wx, _, wst = O.newton_solve("dd", n, want, p4)
+        assert np.array_equal(st, wst) and np.array_equal(x.view(np.uint64), wx.view(np.uint64)), (n, m, k, d)
+        p2 = np.stack([z.real, z.imag], -1)
+        x2, _, st2 = ctx.newton_host(p2, "d")
+        wx2, _, wst2 = O.newton_solve("d", n, O.evaluate("d", S, p2), p2)
+        assert np.array_equal(st2, wst2) and np.array_equal(x2.view(np.uint64), wx2.view(np.uint64)), (n, m, k, d)
