@@ -6,11 +6,13 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <random>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/polyjac_b200.h"
@@ -128,7 +130,172 @@ struct ModeState {
     int over_threads = 0, over_tp = 0, over_variant = 0;
 };
 
+// ------------------------------------------------------------------ shared-memory bank model
+// The fast dd kernel's gathers are 16-byte shared-memory loads (LDS.128) at data-dependent
+// addresses. Model (calibrated against ncu's L1 shared wavefronts of the fast kernel: 2.57x
+// ideal measured, 2.57x modelled): a warp access is served per quarter-warp (8 lanes); a
+// quarter costs the largest number of distinct 16-byte addresses falling into one bank quad
+// (address mod 8). addr[] in 16-byte units, < 0 = lane inactive.
+int quarter_cost(const int* addr) {
+    int q[8][8], nq[8] = {};
+    int worst = 0;
+    for (int l = 0; l < 8; ++l) {
+        const int a = addr[l];
+        if (a < 0) continue;
+        const int b = a & 7;
+        bool dup = false;
+        for (int i = 0; i < nq[b]; ++i) dup |= q[b][i] == a;
+        if (!dup) {
+            q[b][nq[b]++] = a;
+            worst = std::max(worst, nq[b]);
+        }
+    }
+    return worst;
+}
 
+// Deterministic hill climb shared by the two orderings below: propose a swap, keep it when the
+// cost of the (at most two) affected quarter-steps does not grow.
+struct Lcg {
+    uint64_t x;
+    uint32_t next(uint32_t bound) {
+        x = x * 6364136223846793005ull + 1442695040888963407ull;
+        return uint32_t((x >> 33) % bound);
+    }
+};
+
+// fn(p) for p in [0, n) over the host's cores (the per-row orderings below are independent)
+template <class F>
+void parallel_rows(int n, F&& fn) {
+    const int nt = std::min(n / 4, int(std::min(32u, std::thread::hardware_concurrency())));
+    if (nt <= 1) {
+        for (int p = 0; p < n; ++p) fn(p);
+        return;
+    }
+    std::atomic<int> next{0};
+    std::vector<std::thread> th;
+    for (int t = 0; t < nt; ++t)
+        th.emplace_back([&] {
+            for (int p; (p = next++) < n;) fn(p);
+        });
+    for (auto& x : th) x.join();
+}
+
+// Fast-kernel variable order of one (row, 32-monomial chunk): per monomial a permutation of
+// its k (position, exponent) pairs such that at every chain step j the lanes of a quarter-warp
+// gather x from distinct bank quads (point table: 16-byte unit = position). The monomial's
+// products commute, so only rounding changes (the fast order's contract).
+// perm[g*k + j] = original index of the variable the kernel visits at step j.
+void order_variables(const int32_t* pos, int gl, int k, int p_seed, std::vector<uint8_t>& perm) {
+    perm.resize(size_t(gl) * k);
+    for (int g = 0; g < gl; ++g)
+        for (int j = 0; j < k; ++j) perm[g * k + j] = uint8_t(j);
+    if (k < 2) return;
+    auto step_cost = [&](int qw, int j) {
+        int a[8];
+        for (int l = 0; l < 8; ++l) {
+            const int g = qw * 8 + l;
+            a[l] = g < gl ? pos[size_t(g) * k + perm[g * k + j]] : -1;
+        }
+        return quarter_cost(a);
+    };
+    Lcg r{uint64_t(p_seed) * 0x9e3779b97f4a7c15ull + 1};
+    const int iters = 12 * gl * k;
+    for (int it = 0; it < iters; ++it) {
+        const int g = int(r.next(uint32_t(gl)));
+        const int a = int(r.next(uint32_t(k)));
+        int b = int(r.next(uint32_t(k - 1)));
+        b += b >= a;
+        const int qw = g / 8;
+        const int before = step_cost(qw, a) + step_cost(qw, b);
+        std::swap(perm[g * k + a], perm[g * k + b]);
+        if (step_cost(qw, a) + step_cost(qw, b) > before) std::swap(perm[g * k + a], perm[g * k + b]);
+    }
+}
+
+// Stage-3 order of one (row, chunk): ent = (output, staging code) in output-major order, cut
+// into 32 runs of Rr. Within an output the order is free in the fast kernel (a sum's
+// association, the contract of DESIGN.md §5); permute it so that the phase-1 loads, the
+// segment-flush stores and the phase-2 reads of the segment partials (left at each segment's
+// last staging slot) hit distinct bank quads (staging code = 16-byte unit).
+void order_stage3(std::vector<std::pair<int, uint32_t>>& ent, int seed) {
+    const int T = int(ent.size());
+    if (T < 2) return;
+    const int Rr = (T + 31) / 32;
+    std::vector<uint8_t> flush(T);  // segment ends: fixed by the output boundaries and the runs
+    for (int i = 0; i < T; ++i) {
+        const int lane_end = std::min(T, (i / Rr + 1) * Rr);
+        flush[i] = i + 1 == lane_end || ent[i + 1].first != ent[i].first;
+    }
+    // phase-2 groups: the partials read together = same slot (segment ordinal) of the outputs
+    // owned as primaries by the lanes of one quarter-warp (o1 = 64*pass + lane, lane < 32)
+    std::vector<int> g2(T, -1);
+    std::vector<std::vector<int>> members;
+    {
+        std::vector<int> ordinal;
+        std::vector<std::vector<int>> key2group;  // [pass*4 + quarter][slot]
+        for (int i = 0; i < T; ++i) {
+            if (!flush[i]) continue;
+            const int o = ent[i].first;
+            if (int(ordinal.size()) <= o) ordinal.resize(o + 1, 0);
+            const int slot = ordinal[o]++;
+            if ((o & 63) >= 32) continue;  // secondary outputs: paired later, not modelled
+            const int key = (o >> 6) * 4 + (o & 31) / 8;
+            if (int(key2group.size()) <= key) key2group.resize(key + 1);
+            auto& v = key2group[key];
+            if (int(v.size()) <= slot) v.resize(slot + 1, -1);
+            if (v[slot] < 0) {
+                v[slot] = int(members.size());
+                members.emplace_back();
+            }
+            g2[i] = v[slot];
+            members[g2[i]].push_back(i);
+        }
+    }
+    auto p1_cost = [&](int qw, int r) {
+        int a[8], f[8];
+        for (int l = 0; l < 8; ++l) {
+            const int i = (qw * 8 + l) * Rr + r;
+            const bool ok = i < T;
+            a[l] = ok ? int(ent[i].second) : -1;
+            f[l] = ok && flush[i] ? a[l] : -1;
+        }
+        return quarter_cost(a) + quarter_cost(f);
+    };
+    auto p2_cost = [&](int g) {
+        if (g < 0) return 0;
+        int a[8] = {-1, -1, -1, -1, -1, -1, -1, -1};
+        const auto& mem = members[g];
+        for (size_t l = 0; l < mem.size() && l < 8; ++l) a[l] = int(ent[mem[l]].second);
+        return quarter_cost(a);
+    };
+    auto cost = [&](int i, int j) {
+        const int qi = (i / Rr) / 8, ri = i % Rr, qj = (j / Rr) / 8, rj = j % Rr;
+        int c = p1_cost(qi, ri) + (qi == qj && ri == rj ? 0 : p1_cost(qj, rj));
+        return c + p2_cost(g2[i]) + (g2[j] == g2[i] ? 0 : p2_cost(g2[j]));
+    };
+    // swappable pairs: two indices of the same output
+    std::vector<int> start(T), len(T);
+    for (int i = 0; i < T;) {
+        int e = i;
+        while (e < T && ent[e].first == ent[i].first) ++e;
+        for (int q = i; q < e; ++q) {
+            start[q] = i;
+            len[q] = e - i;
+        }
+        i = e;
+    }
+    Lcg r{uint64_t(seed) * 0xbf58476d1ce4e5b9ull + 7};
+    const int iters = 12 * T;
+    for (int it = 0; it < iters; ++it) {
+        const int i = int(r.next(uint32_t(T)));
+        if (len[i] < 2) continue;
+        int j = start[i] + int(r.next(uint32_t(len[i] - 1)));
+        j += j >= i;
+        const int before = cost(i, j);
+        std::swap(ent[i].second, ent[j].second);
+        if (cost(i, j) > before) std::swap(ent[i].second, ent[j].second);
+    }
+}
 
 }  // namespace
 
@@ -143,12 +310,13 @@ struct pj_ctx {
     std::vector<uint16_t> gm_ent;
     uint16_t* d_posexp = nullptr;
     uint32_t* d_posexp32 = nullptr;  // wide encoding (n > 256)
+    uint16_t* d_posexpF = nullptr;   // the fast dd kernel's variable order (order_variables)
     bool wide = false;
     int* d_gm_off = nullptr;
     uint16_t* d_gm_ent = nullptr;
     std::vector<uint32_t> sch, seg;  // fast-kernel stage-3 schedule (host copies)
     std::vector<uint16_t> segcode;
-    std::vector<uint32_t> segq;  // [(p*C + c)*(n+1) + o] x 4 words, see pj_ctx_create
+    std::vector<uint32_t> segq;  // [((p*C + c)*npass + pass)*32 + lane] x 4 words, see pj_ctx_create
     uint32_t* d_segq = nullptr;
     uint32_t* d_sch = nullptr;
     uint32_t* d_seg = nullptr;
@@ -185,6 +353,12 @@ struct pj_ctx {
     int* d_nstat[kHostStreams] = {};
     size_t nx_cap = 0, nwork_cap = 0;
 
+    // the fast dd kernel reads its own variable order (same tables otherwise)
+    pjb::DevSystem dev_fast() const {
+        pjb::DevSystem S = dev(1);
+        S.posexp = d_posexpF;
+        return S;
+    }
     pjb::DevSystem dev(int pi) const {
         pjb::DevSystem S;
         S.n = n;
@@ -222,6 +396,7 @@ void free_ctx(pj_ctx* c) {
     cudaSetDevice(c->device);
     cudaFree(c->d_posexp);
     cudaFree(c->d_posexp32);
+    cudaFree(c->d_posexpF);
     cudaFree(c->d_gm_off);
     cudaFree(c->d_gm_ent);
     cudaFree(c->d_sch);
@@ -295,12 +470,12 @@ int choose_launch(pj_ctx* c, int mode) {
         }
     };
     if (mode == kModeDDFast && !c->wide && pjb::fast_supported(c->k) && M.over_variant >= 0) {
-        // smaller tiles measured faster for the fast kernel (finer grid-stride balance)
-        // measured (tools/tune.py): 8-warp CTAs beat more, smaller CTAs at equal residency;
-        // among tiles that keep the residency, the largest (<= 4) is marginally best
-        // measured (tools/tune.py): 8-warp CTAs beat more, smaller CTAs at equal residency;
-        // at equal residency 2-point tiles are best (C1: 0.853 vs 0.851 (1); C3: 0.763 vs 0.72 (4))
-        std::vector<int> ftps = M.over_tp ? tps : std::vector<int>{2, 4, 1};
+        // measured (tools/tune.py, tools/tp_test.py): 8-warp CTAs beat more, smaller CTAs at
+        // equal residency. Tiles: with 3 CTAs per SM (k <= 12) a 3-point tile uses the last
+        // shared-memory slack and cuts the tile barriers per point (C2: 9.30 vs 9.27 M evals/s for
+        // 2 points, 9.22 for 1); at one CTA per SM (k > 12, C3) 2-point tiles stay best (0.961 vs
+        // 0.945 M for 3, 0.957 for 4)
+        std::vector<int> ftps = M.over_tp ? tps : c->k <= 12 ? std::vector<int>{3, 2, 4, 1} : std::vector<int>{2, 4, 1};
         // (k > 12 admits 10-16 warp CTAs via pj_set_launch; measured at C3: 10 warps, 18.0 ms vs
         // 8 warps, 17.1 ms — the automatic choice stays at 8)
         std::vector<int> fnws = M.over_threads ? nws : std::vector<int>{8};
@@ -534,22 +709,87 @@ int pj_ctx_create_ex(const pj_system_desc* sys, int device, int options, pj_ctx*
     // (value terms first, then Jacobian columns), cut into 32 equal runs (one per lane); a segment
     // is a maximal piece of one output inside one run (byte encoding only: the wide encoding
     // always runs the generic kernel)
+    std::vector<uint16_t> posexpF;  // fast dd kernel's variable order (see order_variables)
     if (!wide) {
         const int R = c->k + 1;
+        const int kk = int(k);
+        posexpF.assign(nm * c->kp, 0);
+        std::vector<int32_t> fpos(nm * k);  // positions in the fast kernel's visiting order
+        parallel_rows(n, [&](int p) {
+            std::vector<uint8_t> perm;
+            for (int ch = 0; ch < C; ++ch) {
+                const int gl = std::min(32, c->m - ch * 32);
+                const size_t s0 = size_t(p) * c->m + size_t(ch) * 32;
+                order_variables(c->pos.data() + s0 * k, gl, kk, p * C + ch, perm);
+                for (int g = 0; g < gl; ++g)
+                    for (int j = 0; j < kk; ++j) {
+                        const size_t s = s0 + g;
+                        const int oj = perm[g * kk + j];
+                        posexpF[s * c->kp + j] = posexp[s * c->kp + oj];
+                        fpos[s * k + j] = c->pos[s * k + oj];
+                    }
+            }
+        });
+        // the fast kernel's gather lists: as gm_off/gm_ent, over the visiting order
+        std::vector<int> foff(size_t(n) * C * n + 1, 0);
+        for (int p = 0; p < n; ++p)
+            for (int g = 0; g < c->m; ++g)
+                for (size_t j = 0; j < k; ++j) foff[(size_t(p) * C + g / 32) * n + fpos[(size_t(p) * c->m + g) * k + j] + 1]++;
+        for (size_t i = 0; i + 1 < foff.size(); ++i) foff[i + 1] += foff[i];
+        std::vector<uint16_t> fent(foff.back());
+        {
+            std::vector<int> fill(foff.begin(), foff.end() - 1);
+            for (int p = 0; p < n; ++p)
+                for (int g = 0; g < c->m; ++g)
+                    for (size_t j = 0; j < k; ++j) {
+                        const size_t li = (size_t(p) * C + g / 32) * n + fpos[(size_t(p) * c->m + g) * k + j];
+                        fent[fill[li]++] = uint16_t(j * 32 + (g & 31));
+                    }
+        }
         c->nseg = n + 1 + 32;
         c->sch.assign(size_t(n) * C * R * 32, 0);
         c->seg.assign(size_t(n) * C * (n + 1), 0);
         c->segcode.assign(size_t(n) * C * c->nseg, 0);
-        std::vector<std::pair<int, uint32_t>> ent;  // (output, staging code)
-        for (int p = 0; p < n; ++p)
+        parallel_rows(n, [&](int p) {
+            std::vector<std::pair<int, uint32_t>> ent;  // (output, staging code)
             for (int ch = 0; ch < C; ++ch) {
                 ent.clear();
                 const int gl = std::min(32, c->m - ch * 32);
                 for (int g = 0; g < gl; ++g) ent.push_back({0, uint32_t(c->k * 32 + g)});
+                // primary outputs (o mod 64 < 32) in order; each secondary output is then inserted
+                // at the first output boundary where all its entries fall into one run, so phase 2
+                // reads it as a single partial (falls back to the end)
+                int Tall = gl;
                 for (int v = 0; v < n; ++v) {
                     const size_t li = (size_t(p) * C + ch) * n + v;
-                    for (int e = c->gm_off[li]; e < c->gm_off[li + 1]; ++e) ent.push_back({v + 1, c->gm_ent[e]});
+                    Tall += foff[li + 1] - foff[li];
                 }
+                const int Rall = (Tall + 31) / 32;
+                std::vector<int> order;
+                for (int v = 0; v < n; ++v)
+                    if (((v + 1) & 63) < 32) order.push_back(v);
+                for (int v = 0; v < n; ++v) {
+                    if (((v + 1) & 63) < 32) continue;
+                    const size_t li = (size_t(p) * C + ch) * n + v;
+                    const int L = foff[li + 1] - foff[li];
+                    int at = int(order.size()), pre = gl;
+                    for (size_t i = 0; i <= order.size() && L > 0; ++i) {
+                        if (pre / Rall == (pre + L - 1) / Rall) {
+                            at = int(i);
+                            break;
+                        }
+                        if (i < order.size()) {
+                            const size_t lj = (size_t(p) * C + ch) * n + order[i];
+                            pre += foff[lj + 1] - foff[lj];
+                        }
+                    }
+                    order.insert(order.begin() + at, v);
+                }
+                for (int v : order) {
+                    const size_t li = (size_t(p) * C + ch) * n + v;
+                    for (int e = foff[li]; e < foff[li + 1]; ++e) ent.push_back({v + 1, fent[e]});
+                }
+                order_stage3(ent, p * C + ch);
                 const int T = int(ent.size());
                 const int Rr = (T + 31) / 32;
                 int segid = -1, prev_o = -1;
@@ -566,24 +806,76 @@ int pj_ctx_create_ex(const pj_system_desc* sys, int device, int options, pj_ctx*
                         }
                         prev_o = o;
                         const bool flush = q + 1 == b || ent[q + 1].first != o;
-                        if (flush) c->segcode[(size_t(p) * C + ch) * c->nseg + segid] = uint16_t(ent[q].second);
+                        // staging slot (j, g) as a 16-byte unit of the warp's staging area: the
+                        // hi pair at 2*unit doubles, rows of 32 slots = 64 units (eval_fast.cu)
+                        const uint32_t unit = (ent[q].second >> 5) * 64 + (ent[q].second & 31);
+                        if (flush) c->segcode[(size_t(p) * C + ch) * c->nseg + segid] = uint16_t(unit);
                         sc[size_t(q - a) * 32 + lane] =
-                            ent[q].second | (uint32_t(segid) << 13) | (flush ? pjb::kSchFlush : 0) | pjb::kSchValid;
+                            unit | (uint32_t(segid) << 13) | (flush ? pjb::kSchFlush : 0) | pjb::kSchValid;
                     }
                 }
             }
-        // per-output 16-byte record for phase 2: first | count << 16 and the first six segment codes
-        // inline (one load per output instead of a dependent code load per segment)
-        c->segq.assign(size_t(n) * C * (n + 1) * 4, 0);
-        for (size_t pc = 0; pc < size_t(n) * C; ++pc)
-            for (int o = 0; o <= n; ++o) {
-                const uint32_t sd = c->seg[pc * (n + 1) + o];
-                const int first = sd & 0xffff, cnt = sd >> 16;
-                uint32_t* q = c->segq.data() + (pc * (n + 1) + o) * 4;
-                q[0] = sd;
-                for (int i = 0; i < std::min(cnt, 6); ++i)
-                    q[1 + i / 2] |= uint32_t(c->segcode[pc * c->nseg + first + i]) << (16 * (i & 1));
+        });
+        // phase-2 records, per (p, c), pass k2 and lane: lane l owns output o1 = 64*k2 + l and at
+        // most one secondary o2 in [64*k2 + 32, 64*k2 + 64), given to the lane with the lightest
+        // load (longest-processing-time order), so one pass covers 64 outputs and the warp's add
+        // slots are the largest per-lane total. Record: {cnt1 | cnt2 << 8 | o2 << 16 (0xffff:
+        // none), six 16-bit segment codes (o1's, then o2's)}; past six, the lane's whole code
+        // list sits in segx at the offset kept in segoff (rare)
+        {
+            const int npass = (n + 64) / 64;
+            std::vector<uint16_t> segx(1, 0);
+            std::vector<uint32_t> segoff(size_t(n) * C * npass * 32, 0);
+            c->segq.assign(size_t(n) * C * npass * 32 * 4, 0);
+            for (size_t pc = 0; pc < size_t(n) * C; ++pc) {
+                auto cnt_of = [&](int o) { return int(c->seg[pc * (n + 1) + o] >> 16); };
+                auto codes_of = [&](int o, std::vector<uint16_t>& dst) {
+                    const uint32_t sd = c->seg[pc * (n + 1) + o];
+                    for (int i = 0; i < int(sd >> 16); ++i) dst.push_back(c->segcode[pc * c->nseg + (sd & 0xffff) + i]);
+                };
+                for (int k2 = 0; k2 < npass; ++k2) {
+                    int load[32], sec[32];
+                    for (int l = 0; l < 32; ++l) {
+                        const int o1 = 64 * k2 + l;
+                        load[l] = o1 <= n ? cnt_of(o1) : 1 << 20;
+                        sec[l] = -1;
+                    }
+                    std::vector<int> extra;
+                    for (int o = 64 * k2 + 32; o <= std::min(n, 64 * k2 + 63); ++o) extra.push_back(o);
+                    std::stable_sort(extra.begin(), extra.end(), [&](int x, int y) { return cnt_of(x) > cnt_of(y); });
+                    for (int o : extra) {
+                        int best = -1;
+                        for (int l = 31; l >= 0; --l)
+                            if (sec[l] < 0 && load[l] < (1 << 20) && (best < 0 || load[l] < load[best])) best = l;
+                        sec[best] = o;
+                        load[best] += cnt_of(o);
+                    }
+                    for (int l = 0; l < 32; ++l) {
+                        const int o1 = 64 * k2 + l;
+                        std::vector<uint16_t> codes;
+                        int c1 = 0, c2 = 0;
+                        if (o1 <= n) {
+                            codes_of(o1, codes);
+                            c1 = int(codes.size());
+                        }
+                        if (sec[l] >= 0) {
+                            codes_of(sec[l], codes);
+                            c2 = int(codes.size()) - c1;
+                        }
+                        const size_t rec = (pc * npass + k2) * 32 + l;
+                        uint32_t* q = c->segq.data() + rec * 4;
+                        q[0] = uint32_t(c1) | uint32_t(c2) << 8 | uint32_t(sec[l] >= 0 ? sec[l] : 0xffff) << 16;
+                        for (int i = 0; i < std::min(int(codes.size()), 6); ++i) q[1 + i / 2] |= uint32_t(codes[i]) << (16 * (i & 1));
+                        if (codes.size() > 6) {
+                            segoff[rec] = uint32_t(segx.size());
+                            segx.insert(segx.end(), codes.begin(), codes.end());
+                        }
+                    }
+                }
             }
+            c->seg.swap(segoff);
+            c->segcode.swap(segx);
+        }
     }
 
     if (device < 0) {  // host-only context: packing and index maps, no device residency
@@ -608,6 +900,7 @@ int pj_ctx_create_ex(const pj_system_desc* sys, int device, int options, pj_ctx*
     if ((e = cudaGetDeviceProperties(&prop, device)) ||
         (e = up((void**)&c->d_posexp, posexp.data(), posexp.size() * 2)) ||
         (e = up((void**)&c->d_posexp32, posexp32.data(), posexp32.size() * 4)) ||
+        (e = up((void**)&c->d_posexpF, posexpF.data(), posexpF.size() * 2)) ||
         (e = up((void**)&c->d_coef[0], cd.data(), cd.size() * 8)) ||
         (e = up((void**)&c->d_coef[1], cdd.data(), cdd.size() * 8)) ||
         (e = up((void**)&c->d_coefT, cddT.data(), cddT.size() * 8)) ||
@@ -683,7 +976,7 @@ int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, d
     cudaGetDevice(&prev);
     if (prev != ctx->device) PJ_CUDA(cudaSetDevice(ctx->device));
     const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
-    cudaError_t e = L.variant == 1 ? pjb::launch_fast(ctx->k, L, ctx->dev(pi), d_points, d_out, (long long)batch,
+    cudaError_t e = L.variant == 1 ? pjb::launch_fast(ctx->k, L, ctx->dev_fast(), d_points, d_out, (long long)batch,
                                                      (cudaStream_t)stream)
                     : L.variant == 2 ? pjb::launch_fastd(ctx->k, L, ctx->dev(pi), d_points, d_out, (long long)batch,
                                                          (cudaStream_t)stream)

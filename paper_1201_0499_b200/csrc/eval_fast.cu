@@ -157,7 +157,7 @@ __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) f
 #pragma unroll
                     for (int r = 0; r < R; ++r) codes[r] = __ldg(sc + r * 32);
                 }
-                const uint4 sq0 = lane <= n ? __ldg(S.segq + pc * (n + 1) + lane) : make_uint4(0u, 0u, 0u, 0u);
+                const uint4 sq0 = __ldg(S.segq + pc * ((n + 64) >> 6) * 32 + lane);
                 // the monomial's coefficient c (lane-minor tile of this (row, chunk))
                 const double* cf = S.coefT + pc * W * 32 + lane;
                 // power-rule scaling a_j * x: d <= 2 means a_j in {1, 2}, an exact scaling of every
@@ -244,8 +244,7 @@ __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) f
                     for (int r = 0; r < R; ++r) {
                         const uint32_t code = codes[r];
                         if (code & kSchValid) {
-                            const int ent = code & 0x1fff;
-                            double* sl = stg + (ent >> 5) * W * 32 + 2 * (ent & 31);
+                            double* sl = stg + 2 * (code & 0x1fff);  // code: 16-byte unit
                             const CDD tv = ld_hl(sl, 64);
                             const DD a = two_sum(sr, tv.rh), b = two_sum(si, tv.ih);
                             sr = a.hi;
@@ -262,36 +261,60 @@ __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) f
                     }
                 }
                 __syncwarp();
-                // ---- stage 3, phase 2: each output adds its (few) segments in order. Output o
-                // goes to lane o for o < 32; the rest are dealt out from lane 31 downwards so the
-                // value (o = 0, the most segments) has lane 0 to itself.
+                // ---- stage 3, phase 2: every output adds its (few) segment partials in order.
+                // Pass k2 covers outputs [64*k2, 64*k2 + 64): lane l owns o1 = 64*k2 + l and at
+                // most one secondary output o2 from the upper half, paired by the host with a
+                // lightly loaded lane (the lane's record lists o1's segment codes, then o2's);
+                // n = 32: 33 outputs in one pass, the value keeps lane 0 to itself
                 const bool last = c + 1 == C;
-                for (int k2 = 0; k2 * 32 <= n; ++k2) {
-                    const int o = k2 == 0 ? lane : 32 * k2 + (31 - lane);
-                    if (o > n) continue;
-                    const uint4 sq = k2 == 0 ? sq0 : __ldg(S.segq + pc * (n + 1) + o);
-                    const int first = sq.x & 0xffff, cnt = sq.x >> 16;
-                    CDD r = c == 0 ? zero : ld_hl(acc + 2 * o, 2 * (n + 1));
-                    const uint32_t pk[3] = {sq.y, sq.z, sq.w};
-#pragma unroll
-                    for (int qq = 0; qq < 6; ++qq) {
-                        if (qq < cnt) {
-                            const int e = (pk[qq >> 1] >> (16 * (qq & 1))) & 0xffff;
-                            const CDD sv = ld_hl(stg + (e >> 5) * W * 32 + 2 * (e & 31), 64);
-                            r = qq == 0 && c == 0 ? sv : cdd_add(r, sv);
-                        }
-                    }
-                    for (int qq = 6; qq < cnt; ++qq) {  // rare: more than six segments
-                        const int e = __ldg(S.segcode + pc * S.nseg + first + qq);
-                        r = cdd_add(r, ld_hl(stg + (e >> 5) * W * 32 + 2 * (e & 31), 64));
-                    }
+                auto INIT = [&](int o) -> CDD { return c == 0 ? zero : ld_hl(acc + 2 * o, 2 * (n + 1)); };
+                auto FIN = [&](int o, const CDD& v) {
                     if (last) {
                         if (t < tp) {
                             const long long at = o == 0 ? p : n + (long long)p * n + (o - 1);
-                            st_aos(out + ((b0 + t) * nout + at) * W, cdd_renorm(r));
+                            st_aos(out + ((b0 + t) * nout + at) * W, cdd_renorm(v));
                         }
                     } else {
-                        st_hl(acc + 2 * o, 2 * (n + 1), r);
+                        st_hl(acc + 2 * o, 2 * (n + 1), v);
+                    }
+                };
+                const int npass = (n + 64) >> 6;
+                for (int k2 = 0; k2 < npass; ++k2) {
+                    const size_t rec = (pc * npass + k2) * 32 + lane;
+                    const uint4 sq = k2 == 0 ? sq0 : __ldg(S.segq + rec);
+                    const int o1 = 64 * k2 + lane, o2 = sq.x >> 16;
+                    const int cnt1 = sq.x & 0xff, tot = cnt1 + ((sq.x >> 8) & 0xff);
+                    const bool has1 = o1 <= n, has2 = o2 != 0xffff;
+                    const uint32_t pk[3] = {sq.y, sq.z, sq.w};
+                    const uint16_t* xs = tot > 6 ? S.segcode + __ldg(S.seg + rec) : nullptr;
+                    auto CODE = [&](int qq) -> int {  // qq-th code of the lane's list (dynamic qq)
+                        if (qq >= 6) return __ldg(xs + qq);
+                        const uint32_t w = qq < 2 ? pk[0] : qq < 4 ? pk[1] : pk[2];
+                        return (w >> (16 * (qq & 1))) & 0xffff;
+                    };
+                    auto LDE = [&](int e) -> CDD { return ld_hl(stg + 2 * e, 64); };  // e: 16-byte unit
+                    CDD r = has1 ? INIT(o1) : zero;
+#pragma unroll
+                    for (int qq = 0; qq < 6; ++qq) {
+                        if (qq < cnt1) {
+                            const CDD sv = LDE((pk[qq >> 1] >> (16 * (qq & 1))) & 0xffff);
+                            r = qq == 0 && c == 0 ? sv : cdd_add(r, sv);
+                        }
+                    }
+                    for (int qq = 6; qq < cnt1; ++qq) r = cdd_add(r, LDE(CODE(qq)));  // rare
+                    if (has1) FIN(o1, r);
+                    if (has2) {  // the lane's secondary output (few lanes)
+                        CDD r2;
+                        if (tot == cnt1 + 1 && c == 0) {  // one segment (the host places it so)
+                            r2 = LDE(CODE(cnt1));
+                        } else {
+                            r2 = INIT(o2);
+                            for (int qq = cnt1; qq < tot; ++qq) {
+                                const CDD sv = LDE(CODE(qq));
+                                r2 = qq == cnt1 && c == 0 ? sv : cdd_add(r2, sv);
+                            }
+                        }
+                        FIN(o2, r2);
                     }
                 }
                 __syncwarp();

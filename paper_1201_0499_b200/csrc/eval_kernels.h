@@ -29,17 +29,19 @@ struct DevSystem {
     const uint16_t* gm_ent;
     // balanced stage-3 schedule of the fast kernel (eval_fast.cu), per (row p, chunk c):
     // sch[((p*chunks + c)*(k+1) + r)*32 + lane] = entry r of lane's run: bits 0-12 staging
-    // code j*32 + g, 13-22 segment id, 23 flush (segment ends here), 24 valid;
-    // seg[(p*chunks + c)*(n+1) + o] = first segment of output o | count << 16 (o = 0 value,
-    // o = v+1 Jacobian column v); nseg = segment capacity per (p, c)
+    // slot of (derivative j, monomial g) as the 16-byte unit j*64 + g of the warp's staging area,
+    // 13-22 segment id, 23 flush (segment ends here), 24 valid; the phase-2 codes below use the
+    // same units;
+    // phase-2 records per (p, c), pass k2 < npass = (n + 64)/64 and lane:
+    // segq[((p*chunks + c)*npass + k2)*32 + lane] = {cnt1 | cnt2 << 8 | o2 << 16, six 16-bit
+    // staging codes}: the lane adds the segment partials of output o1 = 64*k2 + lane (cnt1 of
+    // them), then those of its secondary output o2 (0xffff: none); o = 0 is the value, o = v+1
+    // Jacobian column v. Lanes with more than six codes keep their whole list at
+    // segcode + seg[same index] (nseg unused)
     const uint32_t* sch;
     const uint32_t* seg;
     int nseg;
-    // staging code (j*32 + g) of the last entry of every segment, per (p, c): phase 1 leaves the
-    // segment's partial in that staging slot
     const uint16_t* segcode;
-    // per (p, c, output o): {seg word, codes 0|1<<16, codes 2|3<<16, codes 4|5<<16} (first six
-    // segment codes inline)
     const uint4* segq;
     // plain dd coefficients tiled for the fast kernel: component q of monomial
     // g = 32*chunk + lane of row p at coefT[((p*chunks + chunk)*4 + q)*32 + lane] (0 for g >= m)
