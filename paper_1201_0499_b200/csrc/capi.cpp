@@ -217,7 +217,7 @@ void order_variables(const int32_t* pos, int gl, int k, int p_seed, std::vector<
 // association, the contract of DESIGN.md §5); permute it so that the phase-1 loads, the
 // segment-flush stores and the phase-2 reads of the segment partials (left at each segment's
 // last staging slot) hit distinct bank quads (staging code = 16-byte unit).
-void order_stage3(std::vector<std::pair<int, uint32_t>>& ent, int seed) {
+void order_stage3(std::vector<std::pair<int, uint32_t>>& ent, int seed, int iters) {
     const int T = int(ent.size());
     if (T < 2) return;
     const int Rr = (T + 31) / 32;
@@ -268,10 +268,23 @@ void order_stage3(std::vector<std::pair<int, uint32_t>>& ent, int seed) {
         for (size_t l = 0; l < mem.size() && l < 8; ++l) a[l] = int(ent[mem[l]].second);
         return quarter_cost(a);
     };
-    auto cost = [&](int i, int j) {
-        const int qi = (i / Rr) / 8, ri = i % Rr, qj = (j / Rr) / 8, rj = j % Rr;
-        int c = p1_cost(qi, ri) + (qi == qj && ri == rj ? 0 : p1_cost(qj, rj));
-        return c + p2_cost(g2[i]) + (g2[j] == g2[i] ? 0 : p2_cost(g2[j]));
+    // group costs, cached: p1 group qw*Rr + r (loads and flush stores of one quarter-step), then
+    // the phase-2 groups; a proposal re-evaluates only the (at most four) groups it touches
+    const int G1 = 4 * Rr, G = G1 + int(members.size());
+    auto group_cost = [&](int g) { return g < G1 ? p1_cost(g / Rr, g % Rr) : p2_cost(g - G1); };
+    std::vector<int> gcost(G);
+    for (int g = 0; g < G; ++g) gcost[g] = group_cost(g);
+    auto groups_of = [&](int i, int j, int* out) {
+        int cnt = 0;
+        const int cand[4] = {(i / Rr) / 8 * Rr + i % Rr, (j / Rr) / 8 * Rr + j % Rr, g2[i] < 0 ? -1 : G1 + g2[i],
+                             g2[j] < 0 ? -1 : G1 + g2[j]};
+        for (int x : cand) {
+            if (x < 0) continue;
+            bool dup = false;
+            for (int y = 0; y < cnt; ++y) dup |= out[y] == x;
+            if (!dup) out[cnt++] = x;
+        }
+        return cnt;
     };
     // swappable pairs: two indices of the same output
     std::vector<int> start(T), len(T);
@@ -285,15 +298,24 @@ void order_stage3(std::vector<std::pair<int, uint32_t>>& ent, int seed) {
         i = e;
     }
     Lcg r{uint64_t(seed) * 0xbf58476d1ce4e5b9ull + 7};
-    const int iters = 12 * T;
     for (int it = 0; it < iters; ++it) {
         const int i = int(r.next(uint32_t(T)));
         if (len[i] < 2) continue;
         int j = start[i] + int(r.next(uint32_t(len[i] - 1)));
         j += j >= i;
-        const int before = cost(i, j);
+        int gs[4], after[4];
+        const int ng = groups_of(i, j, gs);
+        int before = 0, now = 0;
         std::swap(ent[i].second, ent[j].second);
-        if (cost(i, j) > before) std::swap(ent[i].second, ent[j].second);
+        for (int q = 0; q < ng; ++q) {
+            before += gcost[gs[q]];
+            now += after[q] = group_cost(gs[q]);
+        }
+        if (now > before) {
+            std::swap(ent[i].second, ent[j].second);
+        } else {
+            for (int q = 0; q < ng; ++q) gcost[gs[q]] = after[q];
+        }
     }
 }
 
@@ -750,6 +772,9 @@ int pj_ctx_create_ex(const pj_system_desc* sys, int device, int options, pj_ctx*
         c->sch.assign(size_t(n) * C * R * 32, 0);
         c->seg.assign(size_t(n) * C * (n + 1), 0);
         c->segcode.assign(size_t(n) * C * c->nseg, 0);
+        // hill-climb budget: 48 proposals per term (model, C2: phase-1 load wavefronts 1,662 vs
+        // 1,922 at 12 per term, ideal 1,152), capped at 2^22 proposals per context
+        const int s3_iters = int(std::min<int64_t>(int64_t(48) * 32 * R, (int64_t(1) << 22) / (int64_t(n) * C)));
         parallel_rows(n, [&](int p) {
             std::vector<std::pair<int, uint32_t>> ent;  // (output, staging code)
             for (int ch = 0; ch < C; ++ch) {
@@ -789,7 +814,7 @@ int pj_ctx_create_ex(const pj_system_desc* sys, int device, int options, pj_ctx*
                     const size_t li = (size_t(p) * C + ch) * n + v;
                     for (int e = foff[li]; e < foff[li + 1]; ++e) ent.push_back({v + 1, fent[e]});
                 }
-                order_stage3(ent, p * C + ch);
+                order_stage3(ent, p * C + ch, s3_iters);
                 const int T = int(ent.size());
                 const int Rr = (T + 31) / 32;
                 int segid = -1, prev_o = -1;
