@@ -319,6 +319,45 @@ void order_stage3(std::vector<std::pair<int, uint32_t>>& ent, int seed, int iter
     }
 }
 
+// Column-to-lane assignment of the complex-double fast kernel for one (row, chunk): its stage 3
+// walks Jacobian column v's ascending-g gather list on one lane, so at every step the lanes read
+// nearby g and collide in the same bank quads. Which columns share a quarter-warp is free (the
+// per-column sums, and so the bit-exact reference order, are untouched): a seeded hill climb
+// regroups them. Column 0 stays on lane 0 (it carries the row's value chain across chunks).
+// lists: the chunk's gm_off / gm_ent slice; perm[lane slot] = column.
+void assign_columns(const int* off, const uint16_t* ent, int n, int seed, uint8_t* perm) {
+    for (int v = 0; v < n; ++v) perm[v] = uint8_t(v);
+    if (n <= 8) return;
+    auto group_cost = [&](int r0, int qw) {  // one quarter-warp of round r0, all steps
+        int mx = 0, c = 0;
+        for (int l = 0; l < 8; ++l) {
+            const int vi = r0 + qw * 8 + l;
+            if (vi < n) mx = std::max(mx, off[perm[vi] + 1] - off[perm[vi]]);
+        }
+        for (int it = 0; it < mx; ++it) {
+            int a[8];
+            for (int l = 0; l < 8; ++l) {
+                const int vi = r0 + qw * 8 + l;
+                const int v = vi < n ? perm[vi] : -1;
+                a[l] = v >= 0 && it < off[v + 1] - off[v] ? int(ent[off[v] + it]) : -1;
+            }
+            c += quarter_cost(a);
+        }
+        return c;
+    };
+    Lcg r{uint64_t(seed) * 0x94d049bb133111ebull + 3};
+    const int iters = 48 * n;
+    for (int it = 0; it < iters; ++it) {
+        const int a = 1 + int(r.next(uint32_t(n - 1)));
+        const int b = 1 + int(r.next(uint32_t(n - 1)));
+        const int ga = a / 8, gb = b / 8;
+        if (ga == gb) continue;
+        const int before = group_cost(ga / 4 * 32, ga % 4) + group_cost(gb / 4 * 32, gb % 4);
+        std::swap(perm[a], perm[b]);
+        if (group_cost(ga / 4 * 32, ga % 4) + group_cost(gb / 4 * 32, gb % 4) > before) std::swap(perm[a], perm[b]);
+    }
+}
+
 }  // namespace
 
 struct pj_ctx {
@@ -336,6 +375,7 @@ struct pj_ctx {
     bool wide = false;
     int* d_gm_off = nullptr;
     uint16_t* d_gm_ent = nullptr;
+    int32_t* d_colq = nullptr;  // complex-double kernel's per-lane-slot column records (assign_columns)
     std::vector<uint32_t> sch, seg;  // fast-kernel stage-3 schedule (host copies)
     std::vector<uint16_t> segcode;
     std::vector<uint32_t> segq;  // [((p*C + c)*npass + pass)*32 + lane] x 4 words, see pj_ctx_create
@@ -375,6 +415,12 @@ struct pj_ctx {
     int* d_nstat[kHostStreams] = {};
     size_t nx_cap = 0, nwork_cap = 0;
 
+    // the complex-double fast kernel reads its column-to-lane assignment
+    pjb::DevSystem dev_fastd() const {
+        pjb::DevSystem S = dev(0);
+        S.colq = reinterpret_cast<const int2*>(d_colq);
+        return S;
+    }
     // the fast dd kernel reads its own variable order (same tables otherwise)
     pjb::DevSystem dev_fast() const {
         pjb::DevSystem S = dev(1);
@@ -400,6 +446,7 @@ struct pj_ctx {
         S.nseg = nseg;
         S.segcode = d_segcode;
         S.segq = reinterpret_cast<const uint4*>(d_segq);
+        S.colq = nullptr;
         S.coefT = d_coefT;
         return S;
     }
@@ -421,6 +468,7 @@ void free_ctx(pj_ctx* c) {
     cudaFree(c->d_posexpF);
     cudaFree(c->d_gm_off);
     cudaFree(c->d_gm_ent);
+    cudaFree(c->d_colq);
     cudaFree(c->d_sch);
     cudaFree(c->d_seg);
     cudaFree(c->d_segcode);
@@ -727,6 +775,26 @@ int pj_ctx_create_ex(const pj_system_desc* sys, int device, int options, pj_ctx*
                 }
     }
 
+    // complex-double fast kernel: column-to-lane assignment per (p, c)
+    std::vector<int32_t> colq(wide ? 0 : size_t(n) * C * n * 2, 0);
+    if (!wide) {
+        parallel_rows(n, [&](int p) {
+            std::vector<int> off(n + 1);
+            std::vector<uint8_t> perm(n);
+            for (int ch = 0; ch < C; ++ch) {
+                const size_t b = (size_t(p) * C + ch) * n;
+                const int base = c->gm_off[b];
+                for (int v = 0; v <= n; ++v) off[v] = c->gm_off[b + v] - base;
+                assign_columns(off.data(), c->gm_ent.data() + base, n, p * C + ch, perm.data());
+                for (int i = 0; i < n; ++i) {
+                    const int v = perm[i];
+                    colq[(b + i) * 2] = c->gm_off[b + v];
+                    colq[(b + i) * 2 + 1] = (c->gm_off[b + v + 1] - c->gm_off[b + v]) | (v << 16);
+                }
+            }
+        });
+    }
+
     // fast-kernel stage-3 schedule: per (p, c) the output-major, ascending-g list of staged terms
     // (value terms first, then Jacobian columns), cut into 32 equal runs (one per lane); a segment
     // is a maximal piece of one output inside one run (byte encoding only: the wide encoding
@@ -931,6 +999,7 @@ int pj_ctx_create_ex(const pj_system_desc* sys, int device, int options, pj_ctx*
         (e = up((void**)&c->d_coefT, cddT.data(), cddT.size() * 8)) ||
         (e = up((void**)&c->d_gm_off, c->gm_off.data(), c->gm_off.size() * 4)) ||
         (e = up((void**)&c->d_gm_ent, c->gm_ent.data(), c->gm_ent.size() * 2)) ||
+        (e = up((void**)&c->d_colq, colq.data(), colq.size() * 4)) ||
         (e = up((void**)&c->d_sch, c->sch.data(), c->sch.size() * 4)) ||
         (e = up((void**)&c->d_seg, c->seg.data(), c->seg.size() * 4)) ||
         (e = up((void**)&c->d_segcode, c->segcode.data(), c->segcode.size() * 2)) ||
@@ -1003,7 +1072,7 @@ int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, d
     const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
     cudaError_t e = L.variant == 1 ? pjb::launch_fast(ctx->k, L, ctx->dev_fast(), d_points, d_out, (long long)batch,
                                                      (cudaStream_t)stream)
-                    : L.variant == 2 ? pjb::launch_fastd(ctx->k, L, ctx->dev(pi), d_points, d_out, (long long)batch,
+                    : L.variant == 2 ? pjb::launch_fastd(ctx->k, L, ctx->dev_fastd(), d_points, d_out, (long long)batch,
                                                          (cudaStream_t)stream)
                                      : pjb::launch_eval(pi + 1, order_of(flags), L, ctx->dev(pi), d_points, d_out,
                                                         (long long)batch, (cudaStream_t)stream);

@@ -18,8 +18,9 @@
 //     fused position/exponent words arrive in one 16-byte load; its k+1 coefficients are
 //     prefetched before stage 1 so their L2 latency hides behind the chains;
 //   * stage 3 keeps the reference's ascending-g order per output (a sequential chain per
-//     output), with lane v walking the gather list of Jacobian column v for both points and
-//     lane 0 also running the two m-term value chains in the same loop.
+//     output), with one lane walking the gather list of a Jacobian column for both points
+//     (columns grouped into quarter-warps by the host against bank conflicts) and lane 0 also
+//     running the two m-term value chains in the same loop.
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -255,14 +256,14 @@ __global__ void __launch_bounds__(256, fastd_min_blocks<K>()) fastd_kernel(DevSy
                 // additionally runs the two value chains over the chunk's monomials.
                 const bool last = c + 1 == C;
                 const int gl = min(32, m - c * 32);
-                for (int v = lane; v < n; v += 32) {  // n >= 1: lane 0 always takes v = 0
+                // lane slot vi handles the column the host assigned to it (columns grouped into
+                // quarter-warps against bank conflicts; slot 0 is always column 0): one 8-byte
+                // record {first entry, count | column << 16}
+                for (int vi = lane; vi < n; vi += 32) {  // n >= 1: lane 0 always takes v = 0
+                    const int2 cq = __ldg(S.colq + (size_t)(p * C + c) * n + vi);
+                    const int v = cq.y >> 16;
                     const bool jac = v < n;
-                    int e0 = 0, len = 0;
-                    if (jac) {
-                        const int li = (p * C + c) * n + v;
-                        e0 = __ldg(S.gm_off + li);
-                        len = __ldg(S.gm_off + li + 1) - e0;
-                    }
+                    const int e0 = cq.x, len = cq.y & 0xffff;
                     CD a[kP];
 #pragma unroll
                     for (int u = 0; u < kP; ++u) a[u] = c == 0 || !jac ? zero : ldv(acc + ((v + 1) * kP + u) * W);

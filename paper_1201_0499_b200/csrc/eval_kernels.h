@@ -43,6 +43,10 @@ struct DevSystem {
     int nseg;
     const uint16_t* segcode;
     const uint4* segq;
+    // complex-double fast kernel (eval_fastd.cu): stage-3 work of lane slot i of (p, c) at
+    // colq[(p*chunks + c)*n + i] = {first gm_ent entry, count | column << 16} (column 0 always at
+    // slot 0; the grouping of columns into quarter-warps is chosen against bank conflicts)
+    const int2* colq;
     // plain dd coefficients tiled for the fast kernel: component q of monomial
     // g = 32*chunk + lane of row p at coefT[((p*chunks + chunk)*4 + q)*32 + lane] (0 for g >= m)
     const double* coefT;

@@ -1,5 +1,6 @@
 """Developer A/B timing of library builds on one GPU: alternates the given .so files (loaded
-through PJ_LIB_PATH in fresh subprocesses) and prints C2 / C3 fast dd evals/s per run.
+through PJ_LIB_PATH in fresh subprocesses) and prints C2 / C3 fast dd and C2 complex-double
+evals/s per run.
 
     python tools/ab.py NAME=path/lib.so NAME2=path2/lib.so [--rounds 3]
 """
@@ -15,19 +16,22 @@ import json, sys, torch
 sys.path.insert(0, sys.argv[1])
 import paper_1201_0499_b200 as pj
 res = {}
-for name, (n, m, k, d, B, reps) in {"c2": (32, 32, 8, 2, 65536, 20), "c3": (64, 64, 16, 10, 8192, 10)}.items():
+for name, (n, m, k, d, B, reps) in {"c2": (32, 32, 8, 2, 65536, 20), "c3": (64, 64, 16, 10, 8192, 10),
+                                     "c2d": (32, 32, 8, 2, 65536, 20)}.items():
+    prec = "d" if name.endswith("d") else "dd"
+    conv = (lambda x: __import__("numpy").stack([x.real, x.imag], -1).copy()) if prec == "d" else pj.to_dd
     s = pj.random_system(n, m, k, d, 7)
     ctx = pj.EvaluationContext(s)
-    pts = [torch.from_numpy(pj.to_dd(pj.random_points(n, B, 11 + i))).cuda() for i in range(2)]
-    out = torch.empty((B, n + n * n, 4), dtype=torch.float64, device="cuda")
+    pts = [torch.from_numpy(conv(pj.random_points(n, B, 11 + i))).cuda() for i in range(2)]
+    out = torch.empty((B, n + n * n, 4 if prec == "dd" else 2), dtype=torch.float64, device="cuda")
     for i in range(3):
-        ctx.evaluate_device(pts[i % 2], out, "dd")
+        ctx.evaluate_device(pts[i % 2], out, prec)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     st = torch.cuda.current_stream()
     e0.record(st)
     for i in range(reps):
-        ctx.evaluate_device(pts[i % 2], out, "dd")
+        ctx.evaluate_device(pts[i % 2], out, prec)
     e1.record(st)
     torch.cuda.synchronize()
     res[name] = B * reps / (e0.elapsed_time(e1) * 1e-3)
