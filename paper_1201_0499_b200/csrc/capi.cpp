@@ -552,6 +552,7 @@ int choose_launch(pj_ctx* c, int mode) {
         for (int nw : fnws)
             for (size_t i = 0; i < ftps.size(); ++i) {
                 const int tp = ftps[i];
+                if (nw * 32 > (c->k <= 12 ? 256 : 512)) continue;  // fast_kernel's launch bounds
                 const size_t sm = smem_need_fast(c, nw, tp);
                 if (sm > c->smem_optin) continue;
                 consider(1, nw, tp, sm, pjb::fast_blocks_per_sm(c->k, c->n, c->d, nw * 32, sm), int(ftps.size() - i));
@@ -564,6 +565,7 @@ int choose_launch(pj_ctx* c, int mode) {
         for (int nw : fnws)
             for (size_t i = 0; i < ftps.size(); ++i) {
                 const int tp = ftps[i];
+                if (nw > 8) continue;  // fastd_kernel's launch bounds: 256 threads
                 const size_t sm = pjb::fastd_smem(c->n, c->m, c->k, c->d, nw, tp);
                 if (sm > c->smem_optin) continue;
                 consider(2, nw, tp, sm, pjb::fastd_blocks_per_sm(c->k, c->d, nw * 32, sm), int(ftps.size() - i));
@@ -572,6 +574,7 @@ int choose_launch(pj_ctx* c, int mode) {
     if (best_score < 0) {
         for (int nw : nws)
             for (int tp : tps) {
+                if (nw > 8) continue;  // eval_kernel's launch bounds: 256 threads
                 const size_t sm = smem_need(c, W, nw, tp);
                 if (sm > c->smem_optin) continue;
                 // fewer, fatter tiles (coefficient reuse) as long as a tile has a task per warp
@@ -580,7 +583,7 @@ int choose_launch(pj_ctx* c, int mode) {
     }
     if (best_score < 0) {
         // global-scratch fallback for systems whose tables exceed shared memory
-        const int nw = M.over_threads ? M.over_threads / 32 : 4;
+        const int nw = M.over_threads ? std::min(M.over_threads / 32, 8) : 4;
         const int tp = M.over_tp ? M.over_tp : 1;
         best.variant = -1;
         best.threads = nw * 32;
@@ -1329,12 +1332,21 @@ int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points) {
         return PJ_OK;
     }
     ModeState& M = ctx->mode[mode_of(flags)];
+    const int old_threads = M.over_threads, old_tp = M.over_tp;
     M.over_threads = threads;
     M.over_tp = tile_points;
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(ctx->device);
     int rc = choose_launch(ctx, mode_of(flags));
+    if (!rc && threads > 256 && M.cfg.variant != 1) {
+        // only the fast dd kernel (k > 12) is built for CTAs above 256 threads: keep the
+        // previous shape instead of planning a launch that cannot run
+        M.over_threads = old_threads;
+        M.over_tp = old_tp;
+        choose_launch(ctx, mode_of(flags));
+        rc = fail(PJ_EINVAL, "threads > 256 need the fast dd kernel (k > 12) with tables that fit shared memory");
+    }
     cudaSetDevice(prev);
     if (!rc) g_err.clear();
     return rc;

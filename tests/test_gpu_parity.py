@@ -312,6 +312,25 @@ def test_fast_kernel_wide_ctas_for_large_k(gpu):
             assert np.array_equal(ctx.evaluate_dd(p4).view(np.uint64), base.view(np.uint64))
 
 
+def test_set_launch_refuses_unrunnable_wide_ctas(gpu):
+    # CTAs above 256 threads exist only for the fast dd kernel at k > 12; anything else is
+    # refused up front and the previous launch shape is kept (no failing launch later)
+    s = pj.random_system(32, 32, 8, 2, 7)
+    ctx = pj.EvaluationContext(s)
+    before = ctx.launch("dd")
+    with pytest.raises(ValueError, match="threads > 256"):
+        ctx.set_launch("dd", 384, 1)
+    assert ctx.launch("dd") == before
+    p4 = pj.to_dd(pj.random_points(32, 5, 3))
+    S = sysd_of(s)
+    want, ms = O.evaluate("dd", S, p4, magsum=True)
+    assert dd_rel(ctx.evaluate_dd(p4), want, ms) <= DD_TOL
+    s16 = pj.random_system(64, 64, 16, 10, 7)  # k = 16, n = 64: 12 warps of staging do not fit
+    c16 = pj.EvaluationContext(s16)
+    with pytest.raises(ValueError, match="threads > 256"):
+        c16.set_launch("dd", 384, 1)
+
+
 def test_dd_contract_under_cancellation(gpu):
     """Adversarial inputs: duplicated monomials with opposite coefficients (exact cancellation
     in every stage-3 sum), unit-modulus points (no decay along k = 16 product chains, d = 10),

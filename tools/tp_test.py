@@ -8,7 +8,7 @@ s = pj.random_system(n, m, k, d, 7)
 ctx = pj.EvaluationContext(s)
 pts = [torch.from_numpy(pj.to_dd(pj.random_points(n, B, 11 + i))).cuda() for i in range(2)]
 out = torch.empty((B, n + n * n, 4), dtype=torch.float64, device="cuda")
-for th, tp in ([(256, 2), (256, 3), (256, 1), (256, 4)] if os.environ.get("C3") else [(256, 2), (256, 3)]):
+for th, tp in ([(256, 2), (320, 1), (320, 2), (384, 1), (352, 1), (256, 1)] if os.environ.get("C3") else [(256, 2), (256, 3)]):
     try:
         ctx.set_launch("dd", th, tp)
     except Exception as e:
