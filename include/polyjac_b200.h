@@ -164,7 +164,9 @@ int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double*
                    double* h_points_out, double* h_norms, int32_t* h_status);
 
 /* Advanced: override the launch shape for `flags`' precision (threads per CTA, multiple of 32,
- * <= 256; points per CTA tile). 0 restores the automatic choice. */
+ * <= 256 — up to 384 for the fast dd kernel at k > 12 when its staging fits shared memory;
+ * points per CTA tile). 0 restores the automatic choice. A shape no kernel can run returns
+ * PJ_EINVAL and keeps the previous one. */
 int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points);
 /* Advanced: kernel choice for complex double (PJ_PREC_D) or the fast dd order. 0 = automatic,
  * -1 = the generic kernel (eval_kernels.cu), 1 = the k-specialised kernel (eval_fastd.cu for complex
