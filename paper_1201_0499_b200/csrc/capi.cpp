@@ -7,11 +7,15 @@
 
 #include <algorithm>
 #include <atomic>
+#include <exception>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <random>
 #include <string>
+#include <mutex>
+#include <stdexcept>
+#include <system_error>
 #include <thread>
 #include <vector>
 
@@ -172,12 +176,29 @@ void parallel_rows(int n, F&& fn) {
         return;
     }
     std::atomic<int> next{0};
-    std::vector<std::thread> th;
-    for (int t = 0; t < nt; ++t)
-        th.emplace_back([&] {
+    std::exception_ptr err;
+    std::mutex mu;
+    auto work = [&] {
+        try {
             for (int p; (p = next++) < n;) fn(p);
-        });
+        } catch (...) {  // handed to the calling thread (a worker must not terminate the process)
+            std::lock_guard<std::mutex> g(mu);
+            if (!err) err = std::current_exception();
+            next = n;
+        }
+    };
+    std::vector<std::thread> th;
+    th.reserve(nt);
+    for (int t = 0; t < nt - 1; ++t) {
+        try {
+            th.emplace_back(work);
+        } catch (const std::system_error&) {  // no more threads: the others and the caller finish
+            break;
+        }
+    }
+    work();
     for (auto& x : th) x.join();
+    if (err) std::rethrow_exception(err);
 }
 
 // Fast-kernel variable order of one (row, 32-monomial chunk): per monomial a permutation of
@@ -688,7 +709,23 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
     return pj_ctx_create_ex(sys, device, 0, out);
 }
 
+static int ctx_create_impl(const pj_system_desc* sys, int device, int options, pj_ctx** out);
+
 int pj_ctx_create_ex(const pj_system_desc* sys, int device, int options, pj_ctx** out) {
+    // no C++ exception crosses the C ABI: host allocation failures (tables, the worker threads
+    // of the host orderings) come back as PJ_ENOMEM
+    try {
+        return ctx_create_impl(sys, device, options, out);
+    } catch (const std::bad_alloc&) {
+        if (out) *out = nullptr;
+        return fail(PJ_ENOMEM, "pj_ctx_create: host allocation failed");
+    } catch (const std::exception& e) {
+        if (out) *out = nullptr;
+        return fail(PJ_ENOMEM, std::string("pj_ctx_create: ") + e.what());
+    }
+}
+
+static int ctx_create_impl(const pj_system_desc* sys, int device, int options, pj_ctx** out) {
     if (!out) return fail(PJ_EINVAL, "null output pointer");
     *out = nullptr;
     if (options & ~PJ_CTX_WIDE) return fail(PJ_EINVAL, "unknown context option");
