@@ -268,9 +268,16 @@ __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) f
                 // n = 32: 33 outputs in one pass, the value keeps lane 0 to itself
                 const bool last = c + 1 == C;
                 auto INIT = [&](int o) -> CDD { return c == 0 ? zero : ld_hl(acc + 2 * o, 2 * (n + 1)); };
+                // (k > 12: the point's output row and the row's Jacobian base hoisted out of the
+                // stores — measured +1% at C3; the k <= 12 kernels keep the inline form, which
+                // their register schedule prefers: -2% at C2 otherwise)
+                double* const orow = out + (b0 + t) * nout * W;
+                const int jb = n + p * n - 1;
                 auto FIN = [&](int o, const CDD& v) {
                     if (last) {
-                        if (t < tp) {
+                        if constexpr (K > 12) {
+                            st_aos(orow + (o == 0 ? p : jb + o) * W, cdd_renorm(v));
+                        } else if (t < tp) {
                             const long long at = o == 0 ? p : n + (long long)p * n + (o - 1);
                             st_aos(out + ((b0 + t) * nout + at) * W, cdd_renorm(v));
                         }
