@@ -339,7 +339,7 @@ cudaError_t launch_t(const LaunchCfg& L, const DevSystem& S, const double* pts, 
                      cudaStream_t st) {
     auto kern = fast_kernel<K, NS, D2>;
     if (L.smem_bytes > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem_bytes);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_limit((const void*)kern));
         if (e != cudaSuccess) return e;
     }
     kern<<<L.blocks, L.threads, L.smem_bytes, st>>>(S, pts, out, B, L.tp, L.flag);
@@ -349,7 +349,7 @@ cudaError_t launch_t(const LaunchCfg& L, const DevSystem& S, const double* pts, 
 template <int K, int NS, bool D2>
 int occ_t(int threads, size_t smem) {
     auto kern = fast_kernel<K, NS, D2>;
-    if (smem > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
+    if (smem > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_limit((const void*)kern)))
         return 0;
     int nb = 0;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem) == cudaSuccess ? nb : 0;

@@ -323,7 +323,7 @@ cudaError_t launch_dt(const LaunchCfg& L, const DevSystem& S, const double* pts,
                       cudaStream_t st) {
     auto kern = fastd_kernel<K, D2>;
     if (L.smem_bytes > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.smem_bytes);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_limit((const void*)kern));
         if (e != cudaSuccess) return e;
     }
     kern<<<L.blocks, L.threads, L.smem_bytes, st>>>(S, pts, out, B, L.tp, L.flag);
@@ -332,7 +332,7 @@ cudaError_t launch_dt(const LaunchCfg& L, const DevSystem& S, const double* pts,
 template <int K, bool D2>
 int occ_dt(int threads, size_t smem) {
     auto kern = fastd_kernel<K, D2>;
-    if (smem > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem))
+    if (smem > 48 * 1024 && cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_limit((const void*)kern)))
         return 0;
     int nb = 0;
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, smem) == cudaSuccess ? nb : 0;

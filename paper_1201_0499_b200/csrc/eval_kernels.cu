@@ -229,7 +229,7 @@ static cudaError_t launch_one(const LaunchCfg& L, const DevSystem& S, const doub
                               cudaStream_t st) {
     auto kern = eval_kernel<T, ORDER, GSCR>;
     if (!GSCR && L.smem_bytes > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, L.smem_bytes);
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_limit((const void*)kern));
         if (e != cudaSuccess) return e;
     }
     kern<<<L.blocks, L.threads, GSCR ? 0 : L.smem_bytes, st>>>(S, pts, out, B, L.tp, L.gscratch, L.flag);
@@ -257,6 +257,14 @@ int max_blocks_per_sm(int prec, int order, int threads, size_t smem) {
         e = order == kRef ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_kernel<CDD, kRef, false>, threads, smem)
                           : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_kernel<CDD, kFast, false>, threads, smem);
     return e == cudaSuccess ? nb : 0;
+}
+
+int dyn_smem_limit(const void* f) {
+    int dev = 0, v = 48 * 1024;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaFuncAttributes fa;
+    if (cudaFuncGetAttributes(&fa, f) == cudaSuccess) v -= int(fa.sharedSizeBytes);
+    return v;
 }
 
 // Prime the dynamic-smem attribute so the occupancy query sees the opt-in limit.

@@ -69,6 +69,12 @@ cudaError_t launch_eval(int prec, int order, const LaunchCfg& L, const DevSystem
                         long long B, cudaStream_t st);
 int max_blocks_per_sm(int prec, int order, int threads, size_t smem);
 cudaError_t set_smem_attr(size_t bytes);
+// The dynamic shared-memory limit every kernel's cudaFuncAttributeMaxDynamicSharedMemorySize is
+// set to: the current device's opt-in maximum. The attribute is process-wide per kernel, so a
+// per-launch value would race between contexts planning / launching on other threads (one
+// context lowering it between another's set and launch); one common value cannot. f: the kernel
+// (its static shared memory comes off the limit).
+int dyn_smem_limit(const void* f);
 
 // fast complex-dd kernels (eval_fast.cu), instantiated for k in [2, 16]
 bool fast_supported(int k);

@@ -700,7 +700,7 @@ bool newton_panel_supported(int n) { return n <= 32; }
 
 int newton_blocks_per_sm(int prec, int n, int threads, size_t smem, bool panel) {
     const void* f = fn_of(prec, n, panel);
-    if (smem) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (smem) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_limit(f));
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, threads, smem) != cudaSuccess) return 0;
     return nb;
@@ -712,7 +712,7 @@ cudaError_t launch_newton(int prec, const NewtonArgs& args, int blocks, int thre
     const void* f = fn_of(prec, args.n, panel && !args.gscratch);
     if (cudaError_t e = init_recip()) return e;
     if (smem) {
-        cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_limit(f));
         if (e) return e;
     }
     const long long nb = blocks < args.B ? blocks : args.B;

@@ -312,6 +312,39 @@ def test_fast_kernel_wide_ctas_for_large_k(gpu):
             assert np.array_equal(ctx.evaluate_dd(p4).view(np.uint64), base.view(np.uint64))
 
 
+def test_concurrent_planning_and_launches_of_mixed_shapes(gpu):
+    # contexts of different shapes planned and launched from several threads at once: the
+    # kernels' dynamic shared-memory attribute is process-wide, so no context may leave it below
+    # another's launch (regression: "too many resources requested for launch" under threads)
+    import threading
+    shapes = [(32, 32, 8, 2, 41), (24, 20, 16, 3, 42), (40, 45, 5, 4, 43), (32, 32, 8, 2, 44)]
+    systems = [pj.random_system(*sh) for sh in shapes]
+    pts = [pj.to_dd(pj.random_points(s.n, 67, 50 + i)) for i, s in enumerate(systems)]
+    want = [pj.EvaluationContext(s).evaluate_dd(p) for s, p in zip(systems, pts)]
+    pts_d = [np.stack([z.real, z.imag], -1).copy() for z in (pj.random_points(s.n, 33, 60 + i) for i, s in enumerate(systems))]
+    want_d = [pj.EvaluationContext(s).evaluate_host(p, "d") for s, p in zip(systems, pts_d)]
+    errors = []
+    barrier = threading.Barrier(len(systems))
+
+    def work(i):
+        try:
+            barrier.wait()
+            ctx = pj.EvaluationContext(systems[i])
+            for _ in range(6):
+                assert np.array_equal(ctx.evaluate_dd(pts[i]).view(np.uint64), want[i].view(np.uint64))
+                got_d = ctx.evaluate_host(pts_d[i], "d")
+                assert np.array_equal(got_d.view(np.uint64), want_d[i].view(np.uint64))
+        except Exception as exc:  # surfaced below
+            errors.append(exc)
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(systems))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+
+
 def test_set_launch_refuses_unrunnable_wide_ctas(gpu):
     # CTAs above 256 threads exist only for the fast dd kernel at k > 12; anything else is
     # refused up front and the previous launch shape is kept (no failing launch later)
