@@ -360,7 +360,12 @@ void assign_columns(const int* off, const uint16_t* ent, int n, int seed, uint8_
             for (int l = 0; l < 8; ++l) {
                 const int vi = r0 + qw * 8 + l;
                 const int v = vi < n ? perm[vi] : -1;
-                a[l] = v >= 0 && it < off[v + 1] - off[v] ? int(ent[off[v] + it]) : -1;
+                if (v >= 0 && it < off[v + 1] - off[v]) {
+                    const int e = ent[off[v] + it], j = e >> 5;  // the kernel's row swizzle (5j mod 8)
+                    a[l] = j * 32 + ((e & 31) ^ ((5 * j) & 7));
+                } else {
+                    a[l] = -1;
+                }
             }
             c += quarter_cost(a);
         }

@@ -41,6 +41,8 @@ __device__ __forceinline__ void stv(double* p, const CD& v) { *reinterpret_cast<
 __device__ __forceinline__ CD sel(bool c, const CD& a, const CD& b) { return {c ? a.re : b.re, c ? a.im : b.im}; }
 
 constexpr int kP = 2;  // points per lane
+// staging swizzle of derivative row j (row K, the value terms, is not swizzled)
+__host__ __device__ constexpr int fastd_swz(int j, int K) { return j < K ? (5 * j) & 7 : 0; }
 #ifndef PJB_FASTD_VPER
 #define PJB_FASTD_VPER 2
 #endif
@@ -139,7 +141,9 @@ __global__ void __launch_bounds__(256, fastd_min_blocks<K>()) fastd_kernel(DevSy
                         return e == 0 ? one : ldv(xt[u] + ((e - 1) * n + POS(j)) * W);
                     }
                 };
-                auto SLOT = [&](int j, int u) -> double* { return stg + ((j * kP + u) * 32 + lane) * W; };
+                // derivative rows j < K keep lane g's slot at g ^ swz(j) (a fixed per-row XOR that
+                // spreads the stage-3 column walks over the bank quads); the value row is plain
+                auto SLOT = [&](int j, int u) -> double* { return stg + ((j * kP + u) * 32 + (lane ^ fastd_swz(j, K))) * W; };
 
                 // stage 1: common factor, ref kernels.cpp:45-53 (sequential from j = 0); for k >= 3 it
                 // runs fused with the forward products below (one gather of x_j serves both chains)
@@ -274,7 +278,8 @@ __global__ void __launch_bounds__(256, fastd_min_blocks<K>()) fastd_kernel(DevSy
                     for (int it = 0; it < iters; ++it) {
                         if (it < len) {
                             const int ent = __ldg(S.gm_ent + e0 + it);
-                            const double* sl = stg + ((ent >> 5) * kP * 32 + (ent & 31)) * W;
+                            const int jr = ent >> 5;
+                            const double* sl = stg + (jr * kP * 32 + ((ent & 31) ^ ((5 * jr) & 7))) * W;
 #pragma unroll
                             for (int u = 0; u < kP; ++u) a[u] = cd_add(a[u], ldv(sl + u * 32 * W));
                         }
