@@ -89,3 +89,50 @@ def test_extreme_doubles_and_file_round_trip(tmp_path):
     path = str(tmp_path / "x.sys")
     pj.write_system(s, path)
     assert same(pj.read_system(path), s)
+
+
+@needs_ref
+def test_parser_agrees_with_the_reference_on_mutated_files():
+    """Differential fuzz: random edits of valid files (digits, signs, dots, exponents, comments,
+    blank lines, whitespace, truncation) must give the same outcome as the reference's
+    read_system — the same system bit for bit, or the same "<name>:<line>: <what>" message."""
+    import random
+    rng = random.Random(1201)
+    alphabet = "0123456789.-+eE x#\n\t"
+    bases = [pj.write_system_text(pj.random_system(*shape, 40 + i))
+             for i, shape in enumerate([(1, 1, 1, 1), (3, 2, 2, 5), (4, 3, 3, 2)])]
+    agree = fails = 0
+    for trial in range(3000):
+        text = bases[trial % len(bases)]
+        for _ in range(rng.randint(1, 3)):
+            i = rng.randrange(len(text) + 1)
+            op = rng.random()
+            if op < 0.4:
+                text = text[:i] + rng.choice(alphabet) + text[i:]
+            elif op < 0.8:
+                text = text[:i] + text[i + 1:]
+            elif op < 0.9:
+                text = text[:i]
+            else:
+                text = text[:i] + rng.choice(alphabet) + text[i + 1:]
+        try:
+            want = O.ref_read_system(text)
+            want_err = None
+        except O.RefError as e:
+            want, want_err = None, str(e)
+        try:
+            got = pj.read_system_text(text, "<test>")
+            got_err = None
+        except pj.FormatError as e:
+            got, got_err = None, str(e)
+        if want_err is not None:
+            assert got_err == want_err, (text, want_err, got_err)
+            fails += 1
+        else:
+            assert got_err is None, (text, got_err)
+            assert (got.n, got.m, got.k, got.d) == (want["n"], want["m"], want["k"], want["d"])
+            assert np.array_equal(got.positions.reshape(-1), want["pos"])
+            assert np.array_equal(got.exponents.reshape(-1), want["exps"])
+            assert np.array_equal(got.coeffs.view(np.uint64), want["coeffs"].view(np.uint64))
+        agree += 1
+    assert agree == 3000 and fails > 500
