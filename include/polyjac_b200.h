@@ -46,6 +46,10 @@ extern "C" {
                                oracle's dd restatement); default dd order is the fast one */
 #define PJ_ORDER_FAST 0x20  /* d: allow the fast order (default for d is the reference order) */
 #define PJ_OP_NEWTON 0x100  /* pj_set_launch / pj_get_launch: address the Newton solve kernel */
+#define PJ_VALIDATE 0x200   /* pj_evaluate: check every coordinate first and return PJ_ENONFINITE
+                               without writing any output when one is non-finite (the
+                               reference's throw-before-evaluate, ref src/engine.cpp:183-188);
+                               costs one read of the points and one stream synchronisation */
 
 typedef struct pj_system_desc {
     int32_t n, m, k, d;
@@ -84,11 +88,17 @@ void pj_ctx_destroy(pj_ctx* ctx);
  * `stream` (a cudaStream_t, NULL = legacy default stream). Replaces
  * EvaluationContext::evaluate / evaluate_batch, ref src/engine.cpp:181-260, batched over
  * points. The caller owns both buffers; no allocation happens here. batch == 0 is a no-op.
- * Non-finite coordinates are flagged on device: read with pj_nonfinite_seen. */
+ * Without PJ_VALIDATE the call stays asynchronous: non-finite coordinates are flagged on device
+ * (read and cleared with pj_nonfinite_seen). With PJ_VALIDATE in `flags` the batch is checked
+ * first and rejected with PJ_ENONFINITE before the evaluation is launched.
+ * One context serves one stream at a time (ref include/polyjac/engine.hpp:84-86): systems
+ * whose tables exceed shared memory use per-CTA global scratch slabs of the context. */
 int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, double* d_out, void* stream);
 
 /* Host-buffer convenience: H2D of the points, pj_evaluate, D2H of the results, synchronous.
- * Returns PJ_ENONFINITE (like the reference's throw) when an input coordinate is non-finite. */
+ * Returns PJ_ENONFINITE (like the reference's throw) when an input coordinate is non-finite
+ * (h_out is then unspecified). A flag left by an earlier asynchronous pj_evaluate is cleared on
+ * entry and does not affect this call. */
 int pj_evaluate_host(pj_ctx* ctx, int flags, const double* h_points, int64_t batch, double* h_out);
 
 /* Synchronises `stream`, then reports (and clears) whether any pj_evaluate since the last
@@ -159,7 +169,9 @@ int pj_newton_step(pj_ctx* ctx, int flags, const double* d_points, const double*
                    double* d_work, double* d_points_out, double* d_norms, int32_t* d_status, void* stream);
 /* Host-buffer convenience: `iters` Newton steps per point on device (chunks whose evaluator
  * output stays L2-resident), synchronous; norms/status describe the last step. Returns
- * PJ_ENONFINITE when an input coordinate is non-finite (like pj_evaluate_host). */
+ * PJ_ENONFINITE when an INPUT coordinate is non-finite (checked on the input points only); an
+ * iterate that diverges to non-finite values is reported per point (status 2) and the other
+ * points' results stand. */
 int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double* h_target, int64_t batch, int iters,
                    double* h_points_out, double* h_norms, int32_t* h_status);
 

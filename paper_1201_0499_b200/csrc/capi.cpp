@@ -410,7 +410,8 @@ struct pj_ctx {
     uint32_t* d_seg = nullptr;
     uint16_t* d_segcode = nullptr;
     int nseg = 0;
-    int* d_flag = nullptr;
+    int* d_flag = nullptr;   // [0]: set by the evaluation kernels on a non-finite coordinate;
+                             // [1]: set by the finiteness check (PJ_VALIDATE, pj_newton_host)
     double* d_coef[2] = {};  // coefficient planes: [0] complex double, [1] complex dd
     double* d_coefT = nullptr;  // complex dd, tiled per (row, chunk) for the fast kernel
     ModeState mode[kModes];
@@ -1049,7 +1050,7 @@ static int ctx_create_impl(const pj_system_desc* sys, int device, int options, p
         (e = up((void**)&c->d_seg, c->seg.data(), c->seg.size() * 4)) ||
         (e = up((void**)&c->d_segcode, c->segcode.data(), c->segcode.size() * 2)) ||
         (e = up((void**)&c->d_segq, c->segq.data(), c->segq.size() * 4)) ||
-        (e = cudaMalloc((void**)&c->d_flag, sizeof(int))) || (e = cudaMemset(c->d_flag, 0, sizeof(int)))) {
+        (e = cudaMalloc((void**)&c->d_flag, 2 * sizeof(int))) || (e = cudaMemset(c->d_flag, 0, 2 * sizeof(int)))) {
         free_ctx(c);
         cudaSetDevice(prev);
         return cuda_fail(e, "pj_ctx_create: device upload");
@@ -1115,6 +1116,25 @@ int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, d
     cudaGetDevice(&prev);
     if (prev != ctx->device) PJ_CUDA(cudaSetDevice(ctx->device));
     const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
+    if (flags & PJ_VALIDATE) {
+        // reject before any output is written, like ref src/engine.cpp:183-188: check the batch on
+        // `stream`, read the verdict back (the one synchronisation of this mode)
+        int bad = 0;
+        cudaStream_t st = (cudaStream_t)stream;
+        const long long words = (long long)batch * ctx->n * (pi == 0 ? 2 : 4);
+        cudaError_t ve;
+        if ((ve = cudaMemsetAsync(ctx->d_flag + 1, 0, sizeof(int), st)) ||
+            (ve = pjb::launch_check_finite(d_points, words, ctx->d_flag + 1, ctx->sms, st)) ||
+            (ve = cudaMemcpyAsync(&bad, ctx->d_flag + 1, sizeof(int), cudaMemcpyDeviceToHost, st)) ||
+            (ve = cudaStreamSynchronize(st))) {
+            if (prev != ctx->device) cudaSetDevice(prev);
+            return cuda_fail(ve, "evaluate: finiteness check");
+        }
+        if (bad) {
+            if (prev != ctx->device) cudaSetDevice(prev);
+            return fail(PJ_ENONFINITE, "evaluate: non-finite coordinate");
+        }
+    }
     cudaError_t e = L.variant == 1 ? pjb::launch_fast(ctx->k, L, ctx->dev_fast(), d_points, d_out, (long long)batch,
                                                      (cudaStream_t)stream)
                     : L.variant == 2 ? pjb::launch_fastd(ctx->k, L, ctx->dev_fastd(), d_points, d_out, (long long)batch,
@@ -1170,9 +1190,14 @@ int pj_evaluate_host(pj_ctx* ctx, int flags, const double* h_points, int64_t bat
     chunk = std::min<int64_t>(chunk, std::max<int64_t>(1, int64_t((1ull << 30) / out_pt)));
     chunk = std::min<int64_t>(chunk, batch);
     const int nchunks = int((batch + chunk - 1) / chunk);
-    const int ns = std::min(nchunks, int(pj_ctx::kHostStreams));
+    // a global-scratch launch (tables beyond shared memory) indexes its slabs by CTA: two such
+    // launches must never run concurrently, so those chunks stay on one stream
+    const int ns = L.gscratch ? 1 : std::min(nchunks, int(pj_ctx::kHostStreams));
     DeviceGuard dg;
     PJ_CUDA(dg.enter(ctx->device));
+    // a stale flag from an earlier asynchronous pj_evaluate must not fail this call
+    PJ_CUDA(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->hstream[0]));
+    PJ_CUDA(cudaStreamSynchronize(ctx->hstream[0]));
     if (size_t(chunk) * in_pt > ctx->in_cap || size_t(chunk) * out_pt > ctx->out_cap) {
         for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
             cudaFree(ctx->d_in[i]);
@@ -1529,7 +1554,16 @@ int pj_newton_step(pj_ctx* ctx, int flags, const double* d_points, const double*
     const size_t x_pt = size_t(ctx->n) * W, out_pt = (size_t(ctx->n) * ctx->n + ctx->n) * W;  // doubles
     const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
     const int64_t chunk = std::max<int64_t>(int64_t(L.blocks) * L.tp * 4, 1);
-    if (batch < 2 * chunk)
+    bool gslab = L.gscratch != nullptr;  // per-CTA global slabs: no two launches may overlap
+    {
+        DeviceGuard dg;
+        PJ_CUDA(dg.enter(ctx->device));
+        pj_ctx::NewtonPlan* P = nullptr;
+        const int prc = newton_plan(ctx, pi, &P);
+        if (prc) return prc;
+        gslab = gslab || P->gscr;
+    }
+    if (batch < 2 * chunk || gslab)
         return newton_step_on(ctx, flags, d_points, d_target, batch, d_work, d_points_out, d_norms, d_status,
                               (cudaStream_t)stream);
     int prev = 0;
@@ -1579,15 +1613,26 @@ int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double*
     // chunk, the evaluate + solve of another and the D2H of a third overlap (stream order protects
     // every buffer's reuse)
     const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
+    int rc0 = PJ_OK;
     const int64_t wave = std::max<int64_t>(int64_t(L.blocks) * L.tp, 1);
     int64_t chunk = std::max<int64_t>(std::max<int64_t>(int64_t((96ull << 20) / out_pt), 4 * wave), 1);
     if (chunk > wave) chunk = chunk / wave * wave;
     chunk = std::min<int64_t>(chunk, std::max<int64_t>(1, int64_t((1ull << 30) / out_pt)));  // bounded staging
     chunk = std::min<int64_t>(chunk, batch);
     const int nchunks = int((batch + chunk - 1) / chunk);
-    const int ns = std::min(nchunks, int(pj_ctx::kHostStreams));
     DeviceGuard dg;
     PJ_CUDA(dg.enter(ctx->device));
+    pj_ctx::NewtonPlan* P = nullptr;
+    rc0 = newton_plan(ctx, pi, &P);
+    if (rc0) return rc0;
+    // global-scratch slabs (evaluation tables or Newton matrices beyond shared memory) are indexed
+    // by CTA: such launches must not overlap, so the chunks then run on one stream
+    const int ns = (L.gscratch || P->gscr) ? 1 : std::min(nchunks, int(pj_ctx::kHostStreams));
+    // the input points are checked on their own flag (d_flag[1]); the evaluator's flag (d_flag[0])
+    // is also raised by iterates that diverged to non-finite values — those are reported per point
+    // through status = 2, so it is cleared on entry and on exit
+    PJ_CUDA(cudaMemsetAsync(ctx->d_flag, 0, 2 * sizeof(int), ctx->hstream[0]));
+    PJ_CUDA(cudaStreamSynchronize(ctx->hstream[0]));
     if (size_t(chunk) * x_pt > ctx->nx_cap || size_t(chunk) * out_pt > ctx->nwork_cap) {
         for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
             cudaFree(ctx->d_nx[i]);
@@ -1621,6 +1666,7 @@ int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double*
         if (dt)
             PJ_CUDA(cudaMemcpyAsync(dt, reinterpret_cast<const char*>(h_target) + size_t(b0) * x_pt,
                                     size_t(nb) * x_pt, cudaMemcpyHostToDevice, st));
+        PJ_CUDA(pjb::launch_check_finite(dx, (long long)nb * ctx->n * W, ctx->d_flag + 1, ctx->sms, st));
         for (int it = 0; it < iters && rc == PJ_OK; ++it)
             rc = newton_step_on(ctx, flags, dx, dt, nb, ctx->d_nwork[si], dx, ctx->d_nnorm[si], ctx->d_nstat[si], st);
         if (rc) break;
@@ -1637,12 +1683,11 @@ int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double*
         cudaError_t e = cudaStreamSynchronize(ctx->hstream[i]);
         if (e && rc == PJ_OK) rc = cuda_fail(e, "newton_host: stream");
     }
-    cudaStream_t st = ctx->hstream[0];
     if (rc) return rc;
     int seen = 0;
-    rc = pj_nonfinite_seen(ctx, st, &seen);
-    if (rc) return rc;
-    if (seen) return fail(PJ_ENONFINITE, "evaluate: non-finite coordinate");
+    PJ_CUDA(cudaMemcpy(&seen, ctx->d_flag + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    PJ_CUDA(cudaMemset(ctx->d_flag, 0, 2 * sizeof(int)));
+    if (seen) return fail(PJ_ENONFINITE, "newton: non-finite input coordinate");
     g_err.clear();
     return PJ_OK;
 }

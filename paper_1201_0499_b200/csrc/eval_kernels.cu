@@ -267,6 +267,27 @@ int dyn_smem_limit(const void* f) {
     return v;
 }
 
+// Finiteness check of a point batch (pj_evaluate with PJ_VALIDATE, pj_newton_host): grid-stride
+// 16-byte loads, one atomic per warp that saw a non-finite word. HBM-bound (one read of the
+// points); the evaluation kernels keep their own flag for the asynchronous path.
+__global__ void check_finite_kernel(const double2* __restrict__ p, long long count2, int* __restrict__ flag) {
+    bool bad = false;
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < count2; i += (long long)gridDim.x * blockDim.x) {
+        const double2 v = __ldg(p + i);
+        bad |= !isfinite(v.x) || !isfinite(v.y);
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1);
+}
+
+cudaError_t launch_check_finite(const double* pts, long long doubles, int* flag, int sms, cudaStream_t st) {
+    const long long c2 = doubles / 2;  // W is 2 or 4: always an even number of doubles
+    if (c2 <= 0) return cudaSuccess;
+    const long long want = (c2 + 255) / 256;
+    const int blocks = (int)(want < (long long)sms * 8 ? want : (long long)sms * 8);
+    check_finite_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const double2*>(pts), c2, flag);
+    return cudaGetLastError();
+}
+
 // Prime the dynamic-smem attribute so the occupancy query sees the opt-in limit.
 cudaError_t set_smem_attr(size_t bytes) {
     cudaError_t e = cudaSuccess;

@@ -68,6 +68,8 @@ struct LaunchCfg {
 cudaError_t launch_eval(int prec, int order, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out,
                         long long B, cudaStream_t st);
 int max_blocks_per_sm(int prec, int order, int threads, size_t smem);
+// sets *flag |= 1 when any of the `doubles` words at pts is non-finite (points: 16-byte aligned)
+cudaError_t launch_check_finite(const double* pts, long long doubles, int* flag, int sms, cudaStream_t st);
 cudaError_t set_smem_attr(size_t bytes);
 // The dynamic shared-memory limit every kernel's cudaFuncAttributeMaxDynamicSharedMemorySize is
 // set to: the current device's opt-in maximum. The attribute is process-wide per kernel, so a

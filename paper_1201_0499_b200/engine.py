@@ -398,22 +398,38 @@ class EvaluationContext:
         rep = BatchReport(evals, t1 - t0, (t1 - t0) / evals if evals else 0.0, delta)
         return BatchResult(results, rep)
 
-    # ---- device path (torch tensors or raw pointers)
-    def evaluate_device(self, points, out, precision: str = "dd", order: str | None = None, stream=None) -> None:
-        """Asynchronous evaluation of device-resident points. points/out: CUDA tensors (or objects
-        with data_ptr()) of shapes [B, n, W] / [B, n + n*n, W], float64, contiguous; stream: a
-        torch.cuda.Stream, a raw cudaStream_t int, or None (torch's current stream)."""
+    # ---- device path (torch tensors)
+    def _dev_tensor(self, what: str, t, shape, dtype: str = "float64"):
+        """The kernels take raw pointers: reject anything but a contiguous CUDA tensor of the exact
+        shape and dtype on this context's device (a float32 or strided view would be read past its
+        end)."""
+        import torch
+        want = {"float64": torch.float64, "int32": torch.int32}[dtype]
+        if not isinstance(t, torch.Tensor):
+            raise TypeError(f"{what}: expected a torch.Tensor on cuda:{self.device}")
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"{what}: shape {tuple(t.shape)} != {tuple(shape)}")
+        if t.dtype != want:
+            raise TypeError(f"{what}: dtype {t.dtype} != {want}")
+        if t.device.type != "cuda" or t.device.index != self.device:
+            raise ValueError(f"{what}: tensor on {t.device}, context on cuda:{self.device}")
+        if not t.is_contiguous():
+            raise ValueError(f"{what}: tensor must be contiguous")
+        return t.data_ptr()
+
+    def evaluate_device(self, points, out, precision: str = "dd", order: str | None = None, stream=None,
+                        validate: bool = False) -> None:
+        """Asynchronous evaluation of device-resident points. points/out: contiguous float64 CUDA
+        tensors on this context's device, [B, n, W] / [B, n + n*n, W]; stream: a torch.cuda.Stream,
+        a raw cudaStream_t int, or None (torch's current stream). validate=True checks the points
+        first and raises ValueError before anything is written when a coordinate is non-finite
+        (PJ_VALIDATE: one stream synchronisation), like ref src/engine.cpp:183-188."""
         W = 2 if precision == "d" else 4
         B = int(points.shape[0])
-        if tuple(points.shape[1:]) != (self.n, W) or tuple(out.shape) != (B, self.n + self.n * self.n, W):
-            raise ValueError("evaluate_device: shape mismatch")
-        if stream is None:
-            import torch
-            stream = torch.cuda.current_stream(points.device).cuda_stream
-        elif hasattr(stream, "cuda_stream"):
-            stream = stream.cuda_stream
-        check(lib().pj_evaluate(self._h, _flags(precision, order), points.data_ptr(), B, out.data_ptr(),
-                                ctypes.c_void_p(stream)))
+        pp = self._dev_tensor("evaluate_device: points", points, (B, self.n, W))
+        po = self._dev_tensor("evaluate_device: out", out, (B, self.n + self.n * self.n, W))
+        flags = _flags(precision, order) | (_lib.PJ_VALIDATE if validate else 0)
+        check(lib().pj_evaluate(self._h, flags, pp, B, po, ctypes.c_void_p(self._stream(stream, points))))
 
     def nonfinite_seen(self, stream=None) -> bool:
         if hasattr(stream, "cuda_stream"):
@@ -469,12 +485,14 @@ class EvaluationContext:
         W = 2 if precision == "d" else 4
         B = int(points.shape[0])
         n = self.n
-        if tuple(points.shape) != (B, n, W) or tuple(out.shape) != (B, n, W) or \
-                tuple(evals.shape) != (B, n + n * n, W) or (target is not None and tuple(target.shape) != (B, n, W)):
-            raise ValueError("newton_solve_device: shape mismatch")
-        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-        check(lib().pj_newton_solve(self._h, _flags(precision, None), evals.data_ptr(), points.data_ptr(), ptr(target),
-                                    B, out.data_ptr(), ptr(norms), ptr(status),
+        what = "newton_solve_device"
+        pe = self._dev_tensor(what + ": evals", evals, (B, n + n * n, W))
+        pp = self._dev_tensor(what + ": points", points, (B, n, W))
+        po = self._dev_tensor(what + ": out", out, (B, n, W))
+        pt = self._dev_tensor(what + ": target", target, (B, n, W)) if target is not None else None
+        pn = self._dev_tensor(what + ": norms", norms, (B, 2)) if norms is not None else None
+        ps = self._dev_tensor(what + ": status", status, (B,), "int32") if status is not None else None
+        check(lib().pj_newton_solve(self._h, _flags(precision, None), pe, pp, pt, B, po, pn, ps,
                                     ctypes.c_void_p(self._stream(stream, points))))
 
     def newton_step_device(self, points, work, out, precision: str = "dd", target=None, norms=None, status=None,
@@ -483,12 +501,14 @@ class EvaluationContext:
         W = 2 if precision == "d" else 4
         B = int(points.shape[0])
         n = self.n
-        if tuple(points.shape) != (B, n, W) or tuple(out.shape) != (B, n, W) or \
-                tuple(work.shape) != (B, n + n * n, W) or (target is not None and tuple(target.shape) != (B, n, W)):
-            raise ValueError("newton_step_device: shape mismatch")
-        ptr = lambda t: t.data_ptr() if t is not None else None  # noqa: E731
-        check(lib().pj_newton_step(self._h, _flags(precision, order), points.data_ptr(), ptr(target), B,
-                                   work.data_ptr(), out.data_ptr(), ptr(norms), ptr(status),
+        what = "newton_step_device"
+        pp = self._dev_tensor(what + ": points", points, (B, n, W))
+        pw = self._dev_tensor(what + ": work", work, (B, n + n * n, W))
+        po = self._dev_tensor(what + ": out", out, (B, n, W))
+        pt = self._dev_tensor(what + ": target", target, (B, n, W)) if target is not None else None
+        pn = self._dev_tensor(what + ": norms", norms, (B, 2)) if norms is not None else None
+        ps = self._dev_tensor(what + ": status", status, (B,), "int32") if status is not None else None
+        check(lib().pj_newton_step(self._h, _flags(precision, order), pp, pt, B, pw, po, pn, ps,
                                    ctypes.c_void_p(self._stream(stream, points))))
 
     # ---- index maps (bit-exact with the reference)
