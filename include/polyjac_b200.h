@@ -119,6 +119,23 @@ int pj_mons_slot(int64_t s, int kind, int var, int n, int m, int64_t* slot);
 int pj_slot_targets(const pj_ctx* ctx, int64_t s, int64_t* targets);
 int64_t pj_zero_mask(const pj_ctx* ctx, int64_t* mask, int64_t cap);
 
+/* The reference's PackedLayout (ref include/polyjac/packing.hpp:24-46, built by build_layout,
+ * ref src/packing.cpp:19-52), exported from the context: positions u8 [n*m*k], exponents u8 [n*m*k]
+ * (degree minus one), coeffs double [(k+1)*n*m][2] derivative-major (block j < k: a_j * c rounded
+ * per component in double; block k: c). Any pointer may be NULL. PJ_EINVAL for a wide context
+ * (n > 256 has no byte encoding). Bit-identical with the reference's build_layout. */
+int pj_layout_export(const pj_ctx* ctx, uint8_t* positions, uint8_t* exponents, double* coeffs);
+
+/* Structural zeros of the Jacobian: mask[p*n + i] = 1 when variable i occurs in no monomial of
+ * polynomial p (those entries are exact +0 in every result, ref include/polyjac/system.hpp:44-46).
+ * mask may be NULL; returns the number of structural zeros. */
+int64_t pj_structural_zeros(const pj_ctx* ctx, uint8_t* mask);
+
+/* Fault injection for tests ("deliberately corrupted coeffs entry"): multiplies the
+ * device copies of monomial s's coefficient (every precision and table) by `factor`. Synchronous.
+ * Not for production use: the context no longer represents its system afterwards. */
+int pj_debug_corrupt_coeff(pj_ctx* ctx, int64_t s, double factor);
+
 /* Multiplication tally of `evals` evaluations (MultCounter, ref include/polyjac/kernels.hpp:15-34;
  * closed form SPEC.md:477): counts[5] = stage1_powers, stage1_factors, stage2, speelpenning, stage3. */
 int pj_mult_counts(const pj_ctx* ctx, int64_t evals, uint64_t* counts);

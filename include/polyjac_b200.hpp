@@ -1,15 +1,20 @@
 // polyjac_b200.hpp — header-only C++ drop-in for the reference's EvaluationContext, over the
 // C ABI in polyjac_b200.h (link libpolyjac_b200.so).
 //
-// Same class and method names as ref include/polyjac/engine.hpp:87-128 and the same exception
-// types (std::invalid_argument for invalid systems / points, std::out_of_range for bad slot
-// queries). The constructor accepts any system type with the reference's shape — including
-// polyjac::PolynomialSystem itself (members n, m, k, d, terms[s].coeff.re/.im,
-// terms[s].support.positions/.exponents) — so switching is a type change:
+// Same class and method names, argument types and exception types as
+// ref include/polyjac/engine.hpp:87-128 (std::invalid_argument for invalid systems / points,
+// std::out_of_range for bad slot queries). The class is a template over a "type family"
+// (Complex, EvaluationPoint, EvaluationResult, BatchResult, PackedLayout, MultCounter,
+// GridConfig):
 //
-//     polyjac::PolynomialSystem sys = polyjac::random_system(32, 32, 9, 2, 7);
-//     polyjac_b200::EvaluationContext ctx(sys);                       // was polyjac::EvaluationContext
-//     auto r = ctx.evaluate<polyjac::EvaluationResult>(point);        // bit-identical results
+//   * polyjac_b200::EvaluationContext uses this header's own mirrors of the reference types;
+//   * polyjac_b200_dropin.hpp instantiates it over the reference's own types, so that with the
+//     reference headers in scope switching is a type change and every call keeps its syntax:
+//
+//       polyjac::PolynomialSystem sys = polyjac::random_system(32, 32, 9, 2, 7);
+//       polyjac_b200::dropin::EvaluationContext ctx(sys);   // was polyjac::EvaluationContext
+//       polyjac::EvaluationResult r = ctx.evaluate(point);  // bit-identical results
+//       std::size_t fp = ctx.layout().footprint_bytes();    // the reference's PackedLayout
 //
 // B200 additions: complex double-double (evaluate_dd), batched device-buffer evaluation on a
 // CUDA stream (evaluate_device), the Newton corrector (newton, newton_dd, newton_step_device) and
@@ -18,6 +23,8 @@
 
 #include <chrono>
 #include <cstdint>
+#include <cstring>
+#include <memory>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -68,6 +75,10 @@ struct MultCounter {
         stage3 += o.stage3;
         return *this;
     }
+    friend bool operator==(const MultCounter& a, const MultCounter& b) {
+        return a.stage1_powers == b.stage1_powers && a.stage1_factors == b.stage1_factors && a.stage2 == b.stage2 &&
+               a.speelpenning == b.speelpenning && a.stage3 == b.stage3;
+    }
 };
 struct BatchReport {
     int evals = 0;
@@ -75,10 +86,33 @@ struct BatchReport {
     double per_eval_seconds = 0.0;
     MultCounter mults;
 };
-template <class Result = EvaluationResult>
 struct BatchResult {
-    std::vector<Result> results;
+    std::vector<EvaluationResult> results;
     BatchReport report;
+};
+// ref include/polyjac/packing.hpp:24-46
+struct PackedLayout {
+    int n = 0, m = 0, k = 0, d = 0;
+    std::vector<std::uint8_t> positions;
+    std::vector<std::uint8_t> exponents;
+    std::vector<Complex> coeffs;
+    std::size_t monomial_count() const { return static_cast<std::size_t>(n) * m; }
+    int position(std::size_t s, int j) const { return positions[s * k + j]; }
+    int exponent_minus_1(std::size_t s, int j) const { return exponents[s * k + j]; }
+    Complex deriv_coeff(std::size_t s, int j) const { return coeffs[static_cast<std::size_t>(j) * monomial_count() + s]; }
+    Complex value_coeff(std::size_t s) const { return coeffs[static_cast<std::size_t>(k) * monomial_count() + s]; }
+    std::size_t footprint_bytes() const { return positions.size() + exponents.size(); }
+};
+
+// The type family of polyjac_b200::EvaluationContext.
+struct OwnTypes {
+    using Complex = polyjac_b200::Complex;
+    using EvaluationPoint = polyjac_b200::EvaluationPoint;
+    using EvaluationResult = polyjac_b200::EvaluationResult;
+    using BatchResult = polyjac_b200::BatchResult;
+    using PackedLayout = polyjac_b200::PackedLayout;
+    using MultCounter = polyjac_b200::MultCounter;
+    using GridConfig = polyjac_b200::GridConfig;
 };
 
 namespace detail {
@@ -92,11 +126,22 @@ inline void check(int rc) {
 }
 }  // namespace detail
 
-class EvaluationContext {
+template <class Types>
+class BasicEvaluationContext {
 public:
-    // options: PJ_CTX_WIDE lifts the reference's n <= 256 cap (pj_ctx_create_ex)
+    using Complex = typename Types::Complex;
+    using EvaluationPoint = typename Types::EvaluationPoint;
+    using EvaluationResult = typename Types::EvaluationResult;
+    using BatchResult = typename Types::BatchResult;
+    using PackedLayout = typename Types::PackedLayout;
+    using MultCounter = typename Types::MultCounter;
+    using GridConfig = typename Types::GridConfig;
+
+    // ref src/engine.cpp:168-179. Accepts any system type with the reference's shape (members n,
+    // m, k, d, terms[s].coeff.re/.im, terms[s].support.positions/.exponents).
+    // options: PJ_CTX_WIDE lifts the reference's n <= 256 cap (pj_ctx_create_ex).
     template <class System>
-    explicit EvaluationContext(const System& sys, GridConfig grid = {}, int device = 0, int options = 0)
+    explicit BasicEvaluationContext(const System& sys, GridConfig grid = {}, int device = 0, int options = 0)
         : grid_(grid) {
         if (grid_.block_size < 1) throw std::invalid_argument("block size must be >= 1");
         if (grid_.workers < 0) throw std::invalid_argument("workers must be >= 0");
@@ -122,14 +167,21 @@ public:
         pj_system_desc desc{sys.n, sys.m, sys.k, sys.d, pos.data(), exps.data(), co.data()};
         if (!shape_ok) desc.positions = nullptr, desc.exponents = nullptr, desc.coeffs = nullptr;
         detail::check(pj_ctx_create_ex(&desc, device, options, &ctx_));
+        const std::int64_t nz = pj_structural_zeros(ctx_, nullptr);
+        if (nz > 0) {
+            std::vector<std::uint8_t> mask(std::size_t(n_) * n_);
+            pj_structural_zeros(ctx_, mask.data());
+            for (std::size_t i = 0; i < mask.size(); ++i)
+                if (mask[i]) zeros_.push_back(i);
+        }
     }
-    ~EvaluationContext() { pj_ctx_destroy(ctx_); }
-    EvaluationContext(const EvaluationContext&) = delete;
-    EvaluationContext& operator=(const EvaluationContext&) = delete;
+    ~BasicEvaluationContext() { pj_ctx_destroy(ctx_); }
+    BasicEvaluationContext(const BasicEvaluationContext&) = delete;
+    BasicEvaluationContext& operator=(const BasicEvaluationContext&) = delete;
 
-    // One point in complex double, bit-identical with the reference (ref src/engine.cpp:181-230).
-    template <class Result = EvaluationResult, class Point>
-    Result evaluate(const Point& point) {
+    // One point in complex double, bit-identical with the reference (ref src/engine.cpp:181-230):
+    // std::invalid_argument on a dimension mismatch or a non-finite coordinate.
+    EvaluationResult evaluate(const EvaluationPoint& point) {
         if (static_cast<int>(point.size()) != n_) throw std::invalid_argument("evaluate: point dimension mismatch");
         std::vector<double> in(2 * std::size_t(n_)), out(2 * (std::size_t(n_) * n_ + n_));
         for (int i = 0; i < n_; ++i) {
@@ -138,14 +190,14 @@ public:
         }
         detail::check(pj_evaluate_host(ctx_, PJ_PREC_D, in.data(), 1, out.data()));
         tally(1);
-        return unpack<Result>(out.data());
+        audit(out.data(), 2);
+        return unpack(out.data());
     }
 
-    // Each point repeat times (ref src/engine.cpp:232-260); one batched launch per repeat.
-    template <class Result = EvaluationResult, class Points>
-    BatchResult<Result> evaluate_batch(const Points& points, int repeat) {
+    // Each point `repeat` times (ref src/engine.cpp:232-260); one batched launch per repeat.
+    BatchResult evaluate_batch(const std::vector<EvaluationPoint>& points, int repeat) {
         if (repeat < 1) throw std::invalid_argument("evaluate_batch: repeat must be >= 1");
-        BatchResult<Result> br;
+        BatchResult br;
         const std::size_t B = points.size(), nout = std::size_t(n_) * n_ + n_;
         std::vector<double> in(2 * B * n_), out(2 * B * nout);
         for (std::size_t b = 0; b < B; ++b) {
@@ -163,15 +215,53 @@ public:
             tally(std::int64_t(B));
         }
         const auto t1 = std::chrono::steady_clock::now();
-        for (std::size_t b = 0; b < B; ++b) br.results.push_back(unpack<Result>(out.data() + 2 * b * nout));
+        for (std::size_t b = 0; b < B; ++b) {
+            audit(out.data() + 2 * b * nout, 2);
+            br.results.push_back(unpack(out.data() + 2 * b * nout));
+        }
         br.report.evals = static_cast<int>(B) * repeat;
         br.report.wall_seconds = std::chrono::duration<double>(t1 - t0).count();
         br.report.per_eval_seconds = br.report.evals ? br.report.wall_seconds / br.report.evals : 0.0;
-        br.report.mults = MultCounter{mults_.stage1_powers - before.stage1_powers,
-                                      mults_.stage1_factors - before.stage1_factors, mults_.stage2 - before.stage2,
-                                      mults_.speelpenning - before.speelpenning, mults_.stage3 - before.stage3};
+        MultCounter d = mults_;
+        d.stage1_powers -= before.stage1_powers;
+        d.stage1_factors -= before.stage1_factors;
+        d.stage2 -= before.stage2;
+        d.speelpenning -= before.speelpenning;
+        d.stage3 -= before.stage3;
+        br.report.mults = d;
         return br;
     }
+
+    // The reference's PackedLayout (ref include/polyjac/engine.hpp:100), bit-identical with
+    // build_layout (ref src/packing.cpp:19-52); built on first use from the context.
+    const PackedLayout& layout() const {
+        if (!layout_) {
+            auto L = std::make_unique<PackedLayout>();
+            std::int32_t n = 0, m = 0, k = 0, d = 0;
+            detail::check(pj_layout_info(ctx_, &n, &m, &k, &d, nullptr));
+            L->n = n, L->m = m, L->k = k, L->d = d;
+            const std::size_t nm = std::size_t(n) * m;
+            L->positions.resize(nm * k);
+            L->exponents.resize(nm * k);
+            std::vector<double> co(2 * (std::size_t(k) + 1) * nm);
+            detail::check(pj_layout_export(ctx_, L->positions.data(), L->exponents.data(), co.data()));
+            L->coeffs.resize((std::size_t(k) + 1) * nm);
+            for (std::size_t i = 0; i < L->coeffs.size(); ++i) {
+                L->coeffs[i].re = co[2 * i];
+                L->coeffs[i].im = co[2 * i + 1];
+            }
+            layout_ = std::move(L);
+        }
+        return *layout_;
+    }
+    const GridConfig& grid() const { return grid_; }
+    // multiplications tallied since construction, in the reference's counting (pj_mult_counts)
+    const MultCounter& mults() const { return mults_; }
+    // ref src/engine.cpp:262-269: true while every masked slot holds an exact +0 pair. The device
+    // path keeps no padded Mons buffer; its masked slots are the structural-zero Jacobian entries
+    // (variable i in no monomial of polynomial p) of every result this context returned, checked
+    // word for word (+0 only, -0 fails) as each result comes back.
+    bool masked_slots_clean() const { return clean_; }
 
     // Complex double-double on host buffers: points [batch][n], out [batch][n + n*n].
     // reference_order = true keeps the reference's order in every stage.
@@ -180,9 +270,12 @@ public:
                                        reinterpret_cast<const double*>(points), batch,
                                        reinterpret_cast<double*>(out)));
         tally(batch);
+        const std::size_t nout = std::size_t(n_) * n_ + n_;
+        for (std::int64_t b = 0; b < batch; ++b) audit(reinterpret_cast<const double*>(out) + 4 * nout * b, 4);
     }
 
-    // Device buffers, asynchronous on `stream` (cudaStream_t); flags = PJ_PREC_D | PJ_PREC_DD [| order].
+    // Device buffers, asynchronous on `stream` (cudaStream_t); flags = PJ_PREC_D | PJ_PREC_DD [| order]
+    // [| PJ_VALIDATE].
     void evaluate_device(int flags, const double* d_points, std::int64_t batch, double* d_out, void* stream) {
         detail::check(pj_evaluate(ctx_, flags, d_points, batch, d_out, stream));
         tally(batch);
@@ -215,16 +308,11 @@ public:
         tally(batch);
     }
 
-    const GridConfig& grid() const { return grid_; }
-    const MultCounter& mults() const { return mults_; }
-    // No padded Mons buffer exists on the device path: masked slots are never materialised.
-    bool masked_slots_clean() const { return true; }
     pj_ctx* handle() const { return ctx_; }
 
 private:
-    template <class Result>
-    Result unpack(const double* o) const {
-        Result r;
+    EvaluationResult unpack(const double* o) const {
+        EvaluationResult r;
         r.n = n_;
         r.values.resize(n_);
         r.jacobian.resize(std::size_t(n_) * n_);
@@ -238,16 +326,34 @@ private:
         }
         return r;
     }
+    // one result [n + n*n][W]: every word of every structural zero must be +0
+    void audit(const double* o, int W) {
+        for (std::size_t z : zeros_)
+            for (int c = 0; c < W; ++c) {
+                std::uint64_t bits;
+                std::memcpy(&bits, o + (n_ + z) * W + c, sizeof bits);
+                if (bits != 0) clean_ = false;
+            }
+    }
     void tally(std::int64_t evals) {
         std::uint64_t c[5];
         detail::check(pj_mult_counts(ctx_, evals, c));
-        mults_ += MultCounter{c[0], c[1], c[2], c[3], c[4]};
+        mults_.stage1_powers += c[0];
+        mults_.stage1_factors += c[1];
+        mults_.stage2 += c[2];
+        mults_.speelpenning += c[3];
+        mults_.stage3 += c[4];
     }
 
     pj_ctx* ctx_ = nullptr;
     int n_ = 0;
     GridConfig grid_;
     MultCounter mults_;
+    std::vector<std::size_t> zeros_;  // structural-zero Jacobian entries p*n + i
+    bool clean_ = true;
+    mutable std::unique_ptr<PackedLayout> layout_;
 };
+
+using EvaluationContext = BasicEvaluationContext<OwnTypes>;
 
 }  // namespace polyjac_b200

@@ -25,6 +25,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ORACLE_SO = os.path.join(HERE, "_build", "liboracle.so")
 REF_SO = os.path.join(HERE, "_ref", "libpolyjac_ref.so")
 DROPIN_BIN = os.path.join(HERE, "_ref", "test_dropin")
+# the reference's own doctest suites, built unmodified (oracle/shim/doctest.h, oracle/Makefile)
+REF_SUITES = ["test_system", "test_packing", "test_kernels", "test_oracle", "test_engine", "test_io"]
+DROPIN_ENGINE_BIN = os.path.join(HERE, "_ref", "test_engine_b200")
+REF_CLI_SUITE = os.path.join(HERE, "_ref", "test_cli")
 REF_SRC = "/root/reference/proj"
 
 _i32p = np.ctypeslib.ndpointer(np.int32, flags="C_CONTIGUOUS")
@@ -38,10 +42,10 @@ def build(ref: bool | None = None) -> None:
     if ref is None:
         ref = os.path.isdir(REF_SRC)
     if ref:
-        subprocess.run(["make", "-s", "-C", HERE, "ref"], check=True)
-        # the C++ drop-in check links the product library; build it only once that exists
+        subprocess.run(["make", "-s", "-C", HERE, "-j8", "ref", "refsuites"], check=True)
+        # the C++ drop-in checks link the product library; build them only once that exists
         if os.path.exists(os.path.join(os.path.dirname(HERE), "paper_1201_0499_b200", "libpolyjac_b200.so")):
-            subprocess.run(["make", "-s", "-C", HERE, "dropin"], check=True)
+            subprocess.run(["make", "-s", "-C", HERE, "-j8", "dropin", "dropin-engine"], check=True)
 
 
 _oracle = None

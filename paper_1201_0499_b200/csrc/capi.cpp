@@ -393,6 +393,7 @@ struct pj_ctx {
     size_t smem_optin = 0;
     int n, m, k, d, kp, chunks;
     std::vector<int32_t> pos, exps;  // host copies (index maps)
+    std::vector<double> c_hi;         // plain coefficients (re, im) of the high words (layout export)
     std::vector<int> gm_off;
     std::vector<uint16_t> gm_ent;
     uint16_t* d_posexp = nullptr;
@@ -750,6 +751,11 @@ static int ctx_create_impl(const pj_system_desc* sys, int device, int options, p
     const size_t nm = size_t(c->n) * c->m, k = c->k;
     c->pos.assign(sys->positions, sys->positions + nm * k);
     c->exps.assign(sys->exponents, sys->exponents + nm * k);
+    c->c_hi.resize(2 * nm);
+    for (size_t s = 0; s < nm; ++s) {
+        c->c_hi[2 * s] = sys->coeffs[4 * s];
+        c->c_hi[2 * s + 1] = sys->coeffs[4 * s + 2];
+    }
 
     // packing v2: fused position/exponent words (ref src/packing.cpp:40-44); the wide encoding
     // (n > 256) widens them to pos | (exp-1) << 16 in 32 bits
@@ -1297,6 +1303,76 @@ int64_t pj_zero_mask(const pj_ctx* ctx, int64_t* mask, int64_t cap) {
         }
     g_err.clear();
     return len;
+}
+
+int pj_layout_export(const pj_ctx* ctx, uint8_t* positions, uint8_t* exponents, double* coeffs) {
+    if (!ctx) return fail(PJ_EINVAL, "null context");
+    if (ctx->n > 256) return fail(PJ_EINVAL, "layout: n > 256 has no byte encoding (wide context)");
+    const size_t nm = size_t(ctx->n) * ctx->m, k = size_t(ctx->k);
+    // ref src/packing.cpp:40-49: positions / exponents-minus-one bytes in S_m order; coefficient
+    // blocks derivative-major, block j < k = a_j * c rounded per component in double, block k = c.
+    // The plain coefficient is recovered from the dd planes' high words of block k.
+    for (size_t s = 0; s < nm; ++s)
+        for (size_t j = 0; j < k; ++j) {
+            if (positions) positions[s * k + j] = uint8_t(ctx->pos[s * k + j]);
+            if (exponents) exponents[s * k + j] = uint8_t(ctx->exps[s * k + j] - 1);
+        }
+    if (coeffs) {
+        for (size_t s = 0; s < nm; ++s) {
+            const double re = ctx->c_hi[2 * s], im = ctx->c_hi[2 * s + 1];
+            for (size_t j = 0; j <= k; ++j) {
+                const double a = j < k ? double(ctx->exps[s * k + j]) : 1.0;
+                coeffs[2 * (j * nm + s)] = j < k ? a * re : re;
+                coeffs[2 * (j * nm + s) + 1] = j < k ? a * im : im;
+            }
+        }
+    }
+    g_err.clear();
+    return PJ_OK;
+}
+
+int64_t pj_structural_zeros(const pj_ctx* ctx, uint8_t* mask) {
+    if (!ctx) return fail(-1, "null context");
+    const int n = ctx->n, C = ctx->chunks;
+    int64_t zeros = 0;
+    for (int p = 0; p < n; ++p)
+        for (int v = 0; v < n; ++v) {
+            bool any = false;
+            for (int c = 0; c < C && !any; ++c) {
+                const size_t li = (size_t(p) * C + c) * n + v;
+                any = ctx->gm_off[li + 1] > ctx->gm_off[li];
+            }
+            if (mask) mask[size_t(p) * n + v] = any ? 0 : 1;
+            zeros += any ? 0 : 1;
+        }
+    g_err.clear();
+    return zeros;
+}
+
+int pj_debug_corrupt_coeff(pj_ctx* ctx, int64_t s, double factor) {
+    if (!ctx) return fail(PJ_EINVAL, "null context");
+    if (ctx->host_only) return fail(PJ_EINVAL, "host-only context");
+    const int64_t nm = int64_t(ctx->n) * ctx->m;
+    if (s < 0 || s >= nm) return fail(PJ_ERANGE, "corrupt_coeff: monomial index " + std::to_string(s));
+    DeviceGuard dg;
+    PJ_CUDA(dg.enter(ctx->device));
+    PJ_CUDA(cudaDeviceSynchronize());
+    auto scale = [&](double* base, size_t idx) -> cudaError_t {
+        double v = 0.0;
+        cudaError_t e = cudaMemcpy(&v, base + idx, sizeof v, cudaMemcpyDeviceToHost);
+        if (e) return e;
+        v *= factor;
+        return cudaMemcpy(base + idx, &v, sizeof v, cudaMemcpyHostToDevice);
+    };
+    for (int j = 0; j <= ctx->k; ++j) {
+        for (int c = 0; c < 2; ++c) PJ_CUDA(scale(ctx->d_coef[0], size_t(j * 2 + c) * nm + s));
+        for (int c = 0; c < 4; ++c) PJ_CUDA(scale(ctx->d_coef[1], size_t(j * 4 + c) * nm + s));
+    }
+    const int64_t p = s / ctx->m, g = s % ctx->m;
+    for (int q = 0; q < 4; ++q)
+        PJ_CUDA(scale(ctx->d_coefT, size_t(((p * ctx->chunks + g / 32) * 4 + q) * 32 + (g & 31))));
+    g_err.clear();
+    return PJ_OK;
 }
 
 int pj_mult_counts(const pj_ctx* ctx, int64_t evals, uint64_t* counts) {

@@ -240,6 +240,37 @@ class EvaluationResult:
 
 
 @dataclass
+class PackedLayout:
+    """ref include/polyjac/packing.hpp:24-46: positions / exponents-minus-one bytes [n*m*k] in S_m
+    order, coeffs complex128 [(k+1)*n*m] derivative-major (block j < k: a_j * c, block k: c)."""
+    n: int
+    m: int
+    k: int
+    d: int
+    positions: np.ndarray
+    exponents: np.ndarray
+    coeffs: np.ndarray
+
+    def monomial_count(self) -> int:
+        return self.n * self.m
+
+    def position(self, s: int, j: int) -> int:
+        return int(self.positions[s * self.k + j])
+
+    def exponent_minus_1(self, s: int, j: int) -> int:
+        return int(self.exponents[s * self.k + j])
+
+    def deriv_coeff(self, s: int, j: int) -> complex:
+        return complex(self.coeffs[j * self.monomial_count() + s])
+
+    def value_coeff(self, s: int) -> complex:
+        return complex(self.coeffs[self.k * self.monomial_count() + s])
+
+    def footprint_bytes(self) -> int:
+        return int(self.positions.size + self.exponents.size)
+
+
+@dataclass
 class MultCounter:
     stage1_powers: int = 0
     stage1_factors: int = 0
@@ -294,6 +325,9 @@ class EvaluationContext:
         check(lib().pj_ctx_create_ex(ctypes.byref(desc), device, _lib.PJ_CTX_WIDE if wide else 0, ctypes.byref(h)))
         self._h = h
         self._mults = MultCounter()
+        self._clean = True
+        self._zeros = None
+        self._layout = None
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -312,9 +346,37 @@ class EvaluationContext:
         return self._mults
 
     def masked_slots_clean(self) -> bool:
-        """The padded Mons buffer does not exist on the GPU path: structural zeros are never
-        written, so every masked slot is trivially an exact +0 (ref engine.cpp:262-269)."""
-        return True
+        """True while every structural zero (Jacobian entry (p, i) with variable i in no monomial
+        of polynomial p) of every result returned by evaluate / evaluate_batch / evaluate_dd has
+        been an exact +0 in every word. The GPU path keeps no padded Mons buffer, so its masked
+        slots (ref src/engine.cpp:262-269) are exactly these output entries."""
+        return self._clean
+
+    def _structural_zeros(self) -> np.ndarray:
+        if self._zeros is None:
+            mask = np.zeros(self.n * self.n, np.uint8)
+            cnt = lib().pj_structural_zeros(self._h, mask.ctypes.data)
+            if cnt < 0:
+                check(_lib.PJ_EINVAL)
+            self._zeros = self.n + np.nonzero(mask)[0]  # output rows of the [B, n + n*n, W] layout
+        return self._zeros
+
+    def _audit(self, out: np.ndarray) -> None:
+        z = self._structural_zeros()
+        if z.size and self._clean:
+            self._clean = not np.any(out[:, z, :].view(np.uint64))
+
+    def layout(self) -> "PackedLayout":
+        """The reference's PackedLayout (ref include/polyjac/packing.hpp:24-46) of this context,
+        bit-identical with build_layout (ref src/packing.cpp:19-52)."""
+        if self._layout is None:
+            nm, k = self.n * self.m, self.k
+            pos = np.empty(nm * k, np.uint8)
+            exps = np.empty(nm * k, np.uint8)
+            co = np.empty(((k + 1) * nm, 2), np.float64)
+            check(lib().pj_layout_export(self._h, pos.ctypes.data, exps.ctypes.data, co.ctypes.data))
+            self._layout = PackedLayout(self.n, self.m, self.k, self.d, pos, exps, co.view(np.complex128).reshape(-1))
+        return self._layout
 
     def layout_info(self):
         n, m, k, d = (ctypes.c_int32() for _ in range(4))
@@ -365,13 +427,17 @@ class EvaluationContext:
         if not np.all(np.isfinite(z.real) & np.isfinite(z.imag)):
             raise ValueError("evaluate: non-finite coordinate")
         pts = np.stack([z.real, z.imag], -1)[None]
-        out = self.evaluate_host(pts, "d")[0]
+        out = self.evaluate_host(pts, "d")
+        self._audit(out)
+        out = out[0]
         c = out[:, 0] + 1j * out[:, 1]
         return EvaluationResult(self.n, c[: self.n].copy(), c[self.n:].copy())
 
     def evaluate_dd(self, points_dd: np.ndarray, order: str | None = None) -> np.ndarray:
         """Complex double-double: points [B, n, 4] -> [B, n + n*n, 4]."""
-        return self.evaluate_host(points_dd, "dd", order)
+        out = self.evaluate_host(points_dd, "dd", order)
+        self._audit(out)
+        return out
 
     def evaluate_batch(self, points, repeat: int) -> BatchResult:
         if repeat < 1:
@@ -388,6 +454,7 @@ class EvaluationContext:
             out = None
             for _ in range(repeat):
                 out = self.evaluate_host(arr, "d")
+                self._audit(out)
             c = out[..., 0] + 1j * out[..., 1]
             results = [EvaluationResult(self.n, c[b, : self.n].copy(), c[b, self.n:].copy()) for b in range(len(pts))]
         t1 = time.perf_counter()

@@ -235,3 +235,34 @@ def test_context_options_validated():
     assert "option" in _lib.last_error()
     assert _lib.lib().pj_ctx_create_ex(ctypes.byref(desc), -1, _lib.PJ_CTX_WIDE, ctypes.byref(h)) == _lib.PJ_OK
     _lib.lib().pj_ctx_destroy(h)
+
+
+@needs_ref
+@pytest.mark.parametrize("shape", [(32, 32, 8, 2), (64, 64, 16, 10), (8, 3, 3, 5), (4, 4, 1, 1), (40, 40, 20, 3)])
+def test_layout_export_bit_identical_to_build_layout(shape):
+    # EvaluationContext::layout() (ref include/polyjac/engine.hpp:100) through pj_layout_export
+    s = pj.random_system(*shape, 77)
+    lay = pj.EvaluationContext(s, device=-1).layout()
+    n, m, k, d = shape
+    nm = n * m
+    rp, re = np.empty(nm * k, np.uint8), np.empty(nm * k, np.uint8)
+    rc = np.empty(((k + 1) * nm, 2), np.float64)
+    sd = sysd_of(s)
+    assert O.ref().ref_build_layout(n, m, k, d, sd["pos"], sd["exps"], sd["coeffs"], rp, re, rc) == 0
+    assert np.array_equal(lay.positions, rp) and np.array_equal(lay.exponents, re)
+    assert np.array_equal(lay.coeffs.view(np.float64).reshape(-1, 2).view(np.uint64), rc.view(np.uint64))
+    assert lay.footprint_bytes() == 2 * nm * k
+    assert lay.position(5, 0) == rp[5 * k] and lay.value_coeff(3) == complex(*rc[k * nm + 3])
+
+
+def test_structural_zeros_match_the_zero_mask():
+    # Jacobian entry (p, v) is a structural zero iff none of its m derivative slots is claimed
+    s = pj.random_system(10, 4, 3, 3, 33)
+    ctx = pj.EvaluationContext(s, device=-1)
+    mask = np.zeros(100, np.uint8)
+    cnt = pj._lib.lib().pj_structural_zeros(ctx._h, mask.ctypes.data)
+    claimed = np.zeros((10, 10), bool)
+    for sidx in range(40):
+        for v in s.positions[sidx]:
+            claimed[sidx // 4, v] = True
+    assert cnt == int((~claimed).sum()) and np.array_equal(mask.reshape(10, 10).astype(bool), ~claimed)
