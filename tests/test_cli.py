@@ -108,3 +108,21 @@ def test_bench_multi_gpu_sharding(gpu):
     assert rc == 0, out
     kv = result_line(out)
     assert kv["gpus"] == str(g) and float(kv["evals_per_s"]) > 1e6
+
+
+@pytest.mark.gpu
+def test_gate_is_independent_of_the_device_pipeline(tmp_path, gpu):
+    # ref SPEC.md:462: a deliberately corrupted coefficient must fail the gate. The corruption is
+    # applied to the DEVICE copies only (pj_debug_corrupt_coeff, both precisions and every table),
+    # so a check that compared the device paths with each other would still pass; the brute-force
+    # host evaluation catches it: check exits 1 and names the polynomial of monomial 37 (p = 6)
+    c = tmp_path / "c.sys"
+    assert run("generate", "--n", 10, "--m", 6, "--k", 4, "--d", 3, "--seed", 12, "--out", c)[0] == 0
+    rc, out = run("check", "--system", c, "--points", 8, "--seed", 4, "--corrupt-coeff", 37)
+    assert rc == 1 and "FAIL" in out and "f[6]" in out, out
+    rc, out = run("bench", "--system", c, "--evals", 3, "--corrupt-coeff", 37)
+    assert rc == 1 and "correctness gate failed" in out, out
+    # unmodified, both pass
+    assert run("check", "--system", c, "--points", 8, "--seed", 4)[0] == 0
+    rc, out = run("bench", "--system", c, "--evals", 3)
+    assert rc == 0 and float(result_line(out)["baseline_ms"]) > 0
