@@ -212,6 +212,9 @@ int pj_get_launch(pj_ctx* ctx, int flags, int32_t* threads, int32_t* tile_points
 /* Measurement helper (not part of the reference surface): FP64 DFMA throughput of `device`
  * in TFLOP/s (2 flops per DFMA), the denominator of the roofline fraction. */
 int pj_fp64_peak_probe(int device, double* tflops);
+/* Measurement helper: issue rate of the FP64 pipe of `device` per operation, lane operations per
+ * second: out[0] DFMA, out[1] DADD, out[2] DMUL (16 independent chains per thread, full grid). */
+int pj_fp64_pipe_probe(int device, double* lane_ops_per_s);
 
 #ifdef __cplusplus
 }

@@ -27,6 +27,7 @@ EXPORTS = [
     "pj_system_read_file", "pj_system_read_text", "pj_system_view", "pj_system_free", "pj_system_write_file",
     "pj_system_write_text", "pj_newton_solve", "pj_newton_step", "pj_newton_host",
     "pj_ctx_create_ex", "pj_layout_export", "pj_structural_zeros", "pj_debug_corrupt_coeff",
+    "pj_fp64_pipe_probe",
 ]
 
 
@@ -90,6 +91,7 @@ def lib():
     L.pj_newton_step.argtypes = [vp, ctypes.c_int, vp, vp, i64, vp, vp, vp, vp, vp]
     L.pj_newton_host.argtypes = [vp, ctypes.c_int, vp, vp, i64, ctypes.c_int, vp, vp, vp]
     L.pj_fp64_peak_probe.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    L.pj_fp64_pipe_probe.argtypes = [ctypes.c_int, vp]
     L.pj_layout_export.argtypes = [vp, vp, vp, vp]
     L.pj_structural_zeros.argtypes = [vp, vp]
     L.pj_structural_zeros.restype = i64

@@ -615,6 +615,13 @@ class EvaluationContext:
         return dict(threads=t.value, tile_points=tp.value, blocks=b.value, smem_bytes=sm.value, variant=var.value)
 
 
+def fp64_pipe_rates(device: int = 0) -> dict:
+    """Issue rate of the FP64 pipe (lane operations / s) for DFMA, DADD and DMUL (pj_fp64_pipe_probe)."""
+    v = (ctypes.c_double * 3)()
+    check(lib().pj_fp64_pipe_probe(device, ctypes.addressof(v)))
+    return {"dfma": v[0], "dadd": v[1], "dmul": v[2]}
+
+
 def fp64_peak_tflops(device: int = 0) -> float:
     v = ctypes.c_double(0)
     check(lib().pj_fp64_peak_probe(device, ctypes.byref(v)))

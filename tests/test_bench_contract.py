@@ -53,8 +53,26 @@ def test_bench_json_line_on_gpu(gpu):
     assert {"bound", "achieved", "peak", "unit", "frac", "traffic"} <= set(roof) and roof["frac"] > 0.5
     assert line["e2e"]["h2d_bytes_per_step"] > 0 and line["e2e"]["d2h_bytes_per_step"] > 0
     assert line["gpu_launches"] == 3 and line["cpu_baseline"]["kind"] == "reference"
-    assert line["parity_gate"]["max_err_over_sum_abs_terms"] <= line["parity_gate"]["tol"]
+    gate = line["parity_gate"]
+    assert gate["pass"] and gate["max_err_over_sum_abs_terms"] <= gate["tol"] and gate["dd_points"] >= 1024
+    assert gate["d_words_differing"] == 0 and gate["structural_zeros_exact"]
     assert line["newton"]["status_ok_frac"] == 1.0
+    assert "c1_latency" in line and line["c1_latency"]["gpu_us_per_eval_d"] > 0
+    assert line["c3"]["config"].startswith("C3") and "65,536" in line["c3"]["config"]
+    # the hardware view is counted in this run (ncu on one untimed launch), not copied from profiles/
+    assert 0.2 < roof["hw_fp64_pipe_frac"] <= 1.0 and roof["traffic"] > 0
+    assert roof["peak"] >= 2 * max(roof["probe_lane_ops_per_s"].values()) / 1e12 * 0.999
+
+
+@pytest.mark.gpu
+def test_bench_exits_nonzero_on_a_broken_kernel(gpu):
+    # a corrupted device coefficient (pj_debug_corrupt_coeff) must fail the gate BEFORE timing:
+    # exit status 3 and no JSON line
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--steps", "3", "--warmup", "3",
+                        "--no-extras", "--no-cpu-baseline", "--no-hw-counts", "--inject-fault"],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 3, r.stderr[-2000:]
+    assert "parity gate FAILED" in r.stderr and not r.stdout.strip()
 
 
 @pytest.mark.gpu
@@ -63,11 +81,16 @@ def test_bench_two_ranks_on_one_gpu(gpu):
     # two ranks sharing the box's GPU over gloo; the driver's N-GPU runs use one GPU per rank + NCCL
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
            "--master-addr", "127.0.0.1", "--master-port", "29533", os.path.join(ROOT, "bench.py"), "--gpus", "2",
-           "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--no-extras", "--dist-backend", "gloo"]
+           "--steps", "3", "--warmup", "3", "--e2e-steps", "1", "--no-extras", "--dist-backend", "gloo",
+           "--global-points", "131072"]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     lines = [ln for ln in r.stdout.strip().splitlines() if ln.startswith("{")]
     assert len(lines) == 1  # rank 0 alone prints
     line = json.loads(lines[0])
-    assert line["n_gpus"] == 2 and line["config"]["global_points"] == 2 * 65536 and line["scaling"] == "weak"
+    assert line["n_gpus"] == 2 and line["config"]["global_points"] == 131072 and line["scaling"] == "strong"
+    assert line["config"]["points_per_gpu"] == 65536 and line["config"]["workload"].startswith("C5")
     assert line["value"] > 1e6 and "cpu_baseline" not in line  # the CPU baseline is N=1 only
+    g = line["gather"]
+    assert g["rank0_rows"] == 131072 and g["own_rows_intact"] and g["bytes_into_rank0"] == 65536 * 1056 * 32
+    assert line["parity_gate"]["pass"]
