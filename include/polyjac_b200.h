@@ -140,6 +140,48 @@ int pj_debug_corrupt_coeff(pj_ctx* ctx, int64_t s, double factor);
  * closed form SPEC.md:477): counts[5] = stage1_powers, stage1_factors, stage2, speelpenning, stage3. */
 int pj_mult_counts(const pj_ctx* ctx, int64_t evals, uint64_t* counts);
 
+/* Ragged systems (non-uniform m and k; the paper's regularity assumption,
+ * ref PAPER.md:258-272, :700-706, lifted). The reference's data model is uniform
+ * (PolynomialSystem n, m, k; ref include/polyjac/system.hpp:14-42); a ragged system keeps its
+ * per-term rules and generalises the shape:
+ *   row_off   int32 [n+1]   polynomial p owns terms [row_off[p], row_off[p+1]); row_off[0] = 0,
+ *                           every polynomial at least one term (m_p >= 1)
+ *   term_off  int32 [T+1]   term t owns slots [term_off[t], term_off[t+1]) of positions/exponents;
+ *                           term_off[0] = 0, 1 <= k_t <= n   (T = row_off[n])
+ *   positions, exponents    int32 [term_off[T]]: 0-based strictly increasing, exponents in [1, d]
+ *   coeffs    double [T][4] (re_hi, re_lo, im_hi, im_lo)
+ * Semantics: the reference's per-term sequence (stage 1 common factor, Speelpenning for the
+ * term's own k_t incl. the k = 1, 2 special cases, ref src/kernels.cpp:45-127), and every output
+ * the ascending-g sum over its polynomial's terms (ref src/kernels.cpp:139-146). A uniform system
+ * written in this form gives bit-identical results to pj_ctx_create's. Output layout unchanged. */
+typedef struct pj_ragged_desc {
+    int32_t n, d;
+    const int32_t* row_off;
+    const int32_t* term_off;
+    const int32_t* positions;
+    const int32_t* exponents;
+    const double* coeffs;
+} pj_ragged_desc;
+/* Violations of the ragged rules (validate_system's wording per term, "polynomial p, monomial g:"
+ * prefix as Violation::describe, ref src/system.cpp:11-19); 0 = valid. */
+int pj_validate_ragged(const pj_ragged_desc* sys, char* msg, size_t cap);
+/* Context for a ragged system: evaluated by the generic kernel (any k_t, m_p; complex double
+ * bit-exact with the oracle's restatement of the reference sequence; dd reference order bit-equal
+ * to the oracle, dd fast order within the §5 tolerance). options: PJ_CTX_WIDE as above. Every
+ * evaluation / Newton entry point accepts the context. pj_layout_info reports m = max m_p,
+ * k = max k_t and footprint 2*sum(k_t); pj_mult_counts and pj_structural_zeros generalise;
+ * the uniform-layout exports (pj_slot_targets, pj_zero_mask, pj_layout_export,
+ * pj_debug_corrupt_coeff) return PJ_EINVAL. */
+int pj_ctx_create_ragged(const pj_ragged_desc* sys, int device, int options, pj_ctx** out);
+/* Deterministic ragged system: m_p uniform in [m_lo, m_hi] per polynomial, k_t uniform in
+ * [k_lo, k_hi] per term, then the reference generator's per-term draws (k_t-subset, exponents
+ * 1 + below(d), coefficient) from the same stream. Two passes: call with NULL arrays to get the
+ * term count *T and slot count *S, then with arrays row_off[n+1], term_off[T+1], positions[S],
+ * exponents[S], coeffs[4T]. */
+int pj_random_ragged_system(int n, int m_lo, int m_hi, int k_lo, int k_hi, int d, uint64_t seed, int64_t* T,
+                            int64_t* S, int32_t* row_off, int32_t* term_off, int32_t* positions, int32_t* exponents,
+                            double* coeffs);
+
 /* Deterministic inputs, bit-identical to random_system / random_points
  * (ref src/system.cpp:66-118, ref src/rng.hpp): coeffs get lo words 0; points are [count][n][2]. */
 int pj_random_system(int n, int m, int k, int d, uint64_t seed, int32_t* positions, int32_t* exponents,

@@ -27,6 +27,7 @@
 //
 // Build (see oracle/Makefile): g++ -O2 -ffp-contract=off; FMA contraction would change the
 // double-mode bits.
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 #include <cstring>
@@ -269,6 +270,78 @@ void evaluate_one(const System& S, const std::vector<T>& dcoef, const std::vecto
     }
 }
 
+// Ragged system (the repo's generalisation, include/polyjac_b200.h
+// pj_ragged_desc): polynomial p owns terms [row_off[p], row_off[p+1]), term t owns
+// [term_off[t], term_off[t+1]) of pos/exps. Literal restatement of the same reference sequence
+// with the shape generalised: the padded Mons buffer has M = max_p m_p rows of S = n^2 + n slots
+// (ref packing.cpp:74-82 with m -> M), term g of polynomial p scatters through the reference's
+// slot map with m -> M (ref packing.cpp:8-17), every stage-3 sum runs over all M rows ascending
+// (ref kernels.cpp:139-146, zero pads included), and each term runs stages 1-2 for its own k_t
+// (ref kernels.cpp:45-127, the k = 1 / k = 2 Speelpenning special cases included).
+struct Ragged {
+    int n, d;
+    const int* row_off;
+    const int* term_off;
+    const int* pos;
+    const int* exps;
+    const double* coeffs;
+};
+template <class T>
+void evaluate_one_ragged(const Ragged& S, const double* point, double* out, double* magsum) {
+    using O = Ops<T>;
+    const int n = S.n, d = S.d;
+    int M = 0;
+    for (int p = 0; p < n; ++p) M = std::max(M, S.row_off[p + 1] - S.row_off[p]);
+    const size_t stride = size_t(n) * n + n;
+    std::vector<T> x(n);
+    for (int i = 0; i < n; ++i) x[i] = O::load(point + size_t(i) * O::W);
+    std::vector<T> pw(size_t(n) * d);
+    for (int i = 0; i < n; ++i) {
+        T* row = pw.data() + size_t(i) * d;
+        row[0] = O::one();
+        if (d >= 2) row[1] = x[i];
+        for (int e = 2; e < d; ++e) row[e] = O::mul(row[e - 1], x[i]);
+    }
+    std::vector<T> mons(stride * M, O::zero());
+    std::vector<double> mmag(magsum ? stride * M : 0, 0.0);
+    Counts c;
+    for (int p = 0; p < n; ++p)
+        for (int t = S.row_off[p]; t < S.row_off[p + 1]; ++t) {
+            const int g = t - S.row_off[p];
+            const int k = S.term_off[t + 1] - S.term_off[t];
+            const int* P = S.pos + S.term_off[t];
+            const int* E = S.exps + S.term_off[t];
+            const T cf = O::coeff(S.coeffs + 4 * size_t(t));
+            std::vector<T> L(k + 1), vals(k);
+            T f = pw[size_t(P[0]) * d + (E[0] - 1)];
+            for (int j = 1; j < k; ++j) f = O::mul(f, pw[size_t(P[j]) * d + (E[j] - 1)]);
+            for (int j = 0; j < k; ++j) vals[j] = x[P[j]];
+            speelpenning(vals.data(), k, L.data(), c);
+            for (int j = 0; j < k; ++j) L[j] = O::mul(L[j], f);
+            L[k] = O::mul(L[k - 1], vals[k - 1]);
+            for (int j = 0; j < k; ++j) L[j] = O::mul(L[j], O::scale(double(E[j]), cf));
+            L[k] = O::mul(L[k], cf);
+            for (int j = 0; j < k; ++j) {
+                const size_t slot = size_t(g) * stride + size_t(P[j] + 1) * n + p;
+                mons[slot] = L[j];
+                if (magsum) mmag[slot] = O::mag(L[j]);
+            }
+            mons[size_t(g) * stride + p] = L[k];
+            if (magsum) mmag[size_t(g) * stride + p] = O::mag(L[k]);
+        }
+    for (size_t t = 0; t < stride; ++t) {
+        T acc = O::zero();
+        double ms = 0.0;
+        for (int j = 0; j < M; ++j) {
+            acc = O::add(acc, mons[t + size_t(j) * stride]);
+            if (magsum) ms += mmag[t + size_t(j) * stride];
+        }
+        const size_t o = t < size_t(n) ? t : n + (t % n) * n + (t / n - 1);
+        O::store(out + o * O::W, acc);
+        if (magsum) magsum[o] = ms;
+    }
+}
+
 template <class T>
 void pack_coeffs(const System& S, std::vector<T>& dcoef, std::vector<T>& vcoef) {
     using O = Ops<T>;
@@ -491,6 +564,34 @@ int oracle_evaluate(int prec, int n, int m, int k, int d, const int* pos, const 
         counts[3] = tot.speel;
         counts[4] = tot.stage3;
     }
+    return 0;
+}
+
+// Ragged evaluation (see evaluate_one_ragged); same buffers as oracle_evaluate.
+int oracle_evaluate_ragged(int prec, int n, int d, const int* row_off, const int* term_off, const int* pos,
+                           const int* exps, const double* coeffs, const double* points, long B, double* out,
+                           double* magsum, int threads) {
+    if (prec != 1 && prec != 2) return 1;
+    oracle::Ragged S{n, d, row_off, term_off, pos, exps, coeffs};
+    const int W = prec == 1 ? 2 : 4;
+    const size_t nout = size_t(n) * n + n;
+    if (threads < 1) threads = 1;
+    if (threads > B) threads = B > 0 ? int(B) : 1;
+    auto work = [&](int t) {
+        for (long b = B * t / threads; b < B * (t + 1) / threads; ++b) {
+            const double* pt = points + size_t(b) * n * W;
+            double* o = out + size_t(b) * nout * W;
+            double* ms = magsum ? magsum + size_t(b) * nout : nullptr;
+            if (prec == 1)
+                oracle::evaluate_one_ragged<oracle::CD>(S, pt, o, ms);
+            else
+                oracle::evaluate_one_ragged<oracle::CDD>(S, pt, o, ms);
+        }
+    };
+    std::vector<std::thread> th;
+    for (int t = 1; t < threads; ++t) th.emplace_back(work, t);
+    work(0);
+    for (auto& t : th) t.join();
     return 0;
 }
 

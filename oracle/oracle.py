@@ -61,6 +61,9 @@ def lib():
         L.oracle_evaluate.argtypes = [ctypes.c_int] * 5 + [_i32p, _i32p, _f64p, _f64p, ctypes.c_long,
                                                            _f64p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int]
         L.oracle_evaluate.restype = ctypes.c_int
+        L.oracle_evaluate_ragged.argtypes = [ctypes.c_int] * 3 + [_i32p] * 4 + [_f64p, _f64p, ctypes.c_long, _f64p,
+                                                                        ctypes.c_void_p, ctypes.c_int]
+        L.oracle_evaluate_ragged.restype = ctypes.c_int
         L.oracle_speelpenning.argtypes = [ctypes.c_int, ctypes.c_int, _f64p, _f64p,
                                           ctypes.POINTER(ctypes.c_ulonglong)]
         L.oracle_cdd_mul.argtypes = [_f64p, _f64p, _f64p]
@@ -142,6 +145,25 @@ def evaluate(prec, sysd, points, threads=1, magsum=False, counts=False):
     if counts:
         res.append(dict(zip(["powers", "factors", "stage2", "speelpenning", "stage3"], list(cnt))))
     return res[0] if len(res) == 1 else tuple(res)
+
+
+def evaluate_ragged(prec, rsys, points, threads=1, magsum=False):
+    """Ragged restatement (oracle.cpp: evaluate_one_ragged). rsys: dict with n, d, row_off [n+1],
+    term_off [T+1], pos, exps [term_off[T]], coeffs [T, 4]."""
+    n, d = rsys["n"], rsys["d"]
+    W = 2 if prec == "d" else 4
+    pts = np.ascontiguousarray(points, dtype=np.float64)
+    B = pts.shape[0]
+    assert pts.shape == (B, n, W), pts.shape
+    out = np.empty((B, n + n * n, W), np.float64)
+    ms = np.empty((B, n + n * n), np.float64) if magsum else None
+    arr = [np.ascontiguousarray(rsys[key], np.int32) for key in ("row_off", "term_off", "pos", "exps")]
+    rc = lib().oracle_evaluate_ragged(1 if prec == "d" else 2, n, d, *arr,
+                                      np.ascontiguousarray(rsys["coeffs"], np.float64).reshape(-1), pts, B, out,
+                                      ms.ctypes.data if ms is not None else None, threads)
+    if rc:
+        raise RuntimeError("oracle_evaluate_ragged failed")
+    return (out, ms) if magsum else out
 
 
 def newton_solve(prec, n, evals, points, target=None, threads=1):

@@ -27,13 +27,19 @@ EXPORTS = [
     "pj_system_read_file", "pj_system_read_text", "pj_system_view", "pj_system_free", "pj_system_write_file",
     "pj_system_write_text", "pj_newton_solve", "pj_newton_step", "pj_newton_host",
     "pj_ctx_create_ex", "pj_layout_export", "pj_structural_zeros", "pj_debug_corrupt_coeff",
-    "pj_fp64_pipe_probe",
+    "pj_fp64_pipe_probe", "pj_validate_ragged", "pj_ctx_create_ragged", "pj_random_ragged_system",
 ]
 
 
 class SystemDesc(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int32), ("m", ctypes.c_int32), ("k", ctypes.c_int32), ("d", ctypes.c_int32),
                 ("positions", ctypes.c_void_p), ("exponents", ctypes.c_void_p), ("coeffs", ctypes.c_void_p)]
+
+
+class RaggedDesc(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int32), ("d", ctypes.c_int32), ("row_off", ctypes.c_void_p),
+                ("term_off", ctypes.c_void_p), ("positions", ctypes.c_void_p), ("exponents", ctypes.c_void_p),
+                ("coeffs", ctypes.c_void_p)]
 
 
 class PolyjacError(RuntimeError):
@@ -96,6 +102,9 @@ def lib():
     L.pj_structural_zeros.argtypes = [vp, vp]
     L.pj_structural_zeros.restype = i64
     L.pj_debug_corrupt_coeff.argtypes = [vp, i64, ctypes.c_double]
+    L.pj_validate_ragged.argtypes = [ctypes.POINTER(RaggedDesc), ctypes.c_char_p, ctypes.c_size_t]
+    L.pj_ctx_create_ragged.argtypes = [ctypes.POINTER(RaggedDesc), ctypes.c_int, ctypes.c_int, ctypes.POINTER(vp)]
+    L.pj_random_ragged_system.argtypes = [ctypes.c_int] * 6 + [u64, i64p, i64p, vp, vp, vp, vp, vp]
     for name in EXPORTS:
         getattr(L, name)  # fail loudly on a stale library
     _lib = L

@@ -392,7 +392,15 @@ struct pj_ctx {
     int sms = 0;
     size_t smem_optin = 0;
     int n, m, k, d, kp, chunks;
-    std::vector<int32_t> pos, exps;  // host copies (index maps)
+    // ragged system (pj_ctx_create_ragged): m = max m_p, k = max k_t, chunks = max chunks per row;
+    // nterms = T; the per-row term / chunk offsets and per-term k below (host and device)
+    bool ragged = false;
+    int64_t nterms = 0;
+    std::vector<int32_t> row_off, row_chunk, term_off;
+    int* d_row_off = nullptr;
+    int* d_row_chunk = nullptr;
+    uint16_t* d_term_k = nullptr;
+    std::vector<int32_t> pos, exps;  // host copies (index maps; ragged: CSR by term_off)
     std::vector<double> c_hi;         // plain coefficients (re, im) of the high words (layout export)
     std::vector<int> gm_off;
     std::vector<uint16_t> gm_ent;
@@ -461,8 +469,11 @@ struct pj_ctx {
         S.m = m;
         S.k = k;
         S.d = d;
-        S.nm = n * m;
+        S.nm = ragged ? int(nterms) : n * m;
         S.chunks = chunks;
+        S.row_off = ragged ? d_row_off : nullptr;
+        S.row_chunk = ragged ? d_row_chunk : nullptr;
+        S.term_k = ragged ? d_term_k : nullptr;
         S.kp = kp;
         S.posexp = d_posexp;
         S.posexp32 = wide ? d_posexp32 : nullptr;
@@ -505,6 +516,9 @@ void free_ctx(pj_ctx* c) {
     cudaFree(c->d_coef[0]);
     cudaFree(c->d_coef[1]);
     cudaFree(c->d_coefT);
+    cudaFree(c->d_row_off);
+    cudaFree(c->d_row_chunk);
+    cudaFree(c->d_term_k);
     cudaFree(c->d_scratch);
     cudaFree(c->d_nscratch);
     for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
@@ -567,7 +581,7 @@ int choose_launch(pj_ctx* c, int mode) {
             best.gscratch = nullptr;
         }
     };
-    if (mode == kModeDDFast && !c->wide && pjb::fast_supported(c->k) && M.over_variant >= 0) {
+    if (mode == kModeDDFast && !c->wide && !c->ragged && pjb::fast_supported(c->k) && M.over_variant >= 0) {
         // measured (tools/tune.py, tools/tp_test.py): 8-warp CTAs beat more, smaller CTAs at
         // equal residency. Tiles: with 3 CTAs per SM (k <= 12) a 3-point tile uses the last
         // shared-memory slack and cuts the tile barriers per point (C2: 9.30 vs 9.27 M evals/s for
@@ -586,7 +600,7 @@ int choose_launch(pj_ctx* c, int mode) {
                 consider(1, nw, tp, sm, pjb::fast_blocks_per_sm(c->k, c->n, c->d, nw * 32, sm), int(ftps.size() - i));
             }
     }
-    if (mode == kModeD && !c->wide && pjb::fastd_supported(c->k) && M.over_variant >= 0) {
+    if (mode == kModeD && !c->wide && !c->ragged && pjb::fastd_supported(c->k) && M.over_variant >= 0) {
         // point pairs per warp: tiles of 2 points per warp (one pair task per warp per row sweep)
         std::vector<int> fnws = M.over_threads ? nws : std::vector<int>{8, 4};
         std::vector<int> ftps = M.over_tp ? tps : std::vector<int>{16, 8, 4, 2};
@@ -606,7 +620,7 @@ int choose_launch(pj_ctx* c, int mode) {
                 const size_t sm = smem_need(c, W, nw, tp);
                 if (sm > c->smem_optin) continue;
                 // fewer, fatter tiles (coefficient reuse) as long as a tile has a task per warp
-                consider(-1, nw, tp, sm, pjb::max_blocks_per_sm(precflag, 0, nw * 32, sm), tp * c->n >= nw ? tp : 0);
+                consider(-1, nw, tp, sm, pjb::max_blocks_per_sm(precflag, 0, nw * 32, sm, c->ragged), tp * c->n >= nw ? tp : 0);
             }
     }
     if (best_score < 0) {
@@ -716,6 +730,7 @@ int pj_ctx_create(const pj_system_desc* sys, int device, pj_ctx** out) {
     return pj_ctx_create_ex(sys, device, 0, out);
 }
 
+struct HostPack;
 static int ctx_create_impl(const pj_system_desc* sys, int device, int options, pj_ctx** out);
 
 int pj_ctx_create_ex(const pj_system_desc* sys, int device, int options, pj_ctx** out) {
@@ -730,6 +745,96 @@ int pj_ctx_create_ex(const pj_system_desc* sys, int device, int options, pj_ctx*
         if (out) *out = nullptr;
         return fail(PJ_ENOMEM, std::string("pj_ctx_create: ") + e.what());
     }
+}
+
+// Device residency shared by the uniform and the ragged context: upload the packed tables once,
+// create the host-API streams, pick every mode's launch shape. Consumes c (freed on failure).
+struct HostPack {
+    std::vector<uint16_t> posexp, posexpF;
+    std::vector<uint32_t> posexp32;
+    std::vector<double> cd, cdd, cddT;
+    std::vector<int32_t> colq;
+    std::vector<uint16_t> term_k;  // ragged only
+};
+static int ctx_upload(pj_ctx* c, int device, const HostPack& hp, pj_ctx** out) {
+    const auto& posexp = hp.posexp;
+    const auto& posexp32 = hp.posexp32;
+    const auto& posexpF = hp.posexpF;
+    const auto& cd = hp.cd;
+    const auto& cdd = hp.cdd;
+    const auto& cddT = hp.cddT;
+    const auto& colq = hp.colq;
+    int rc = PJ_OK;
+    if (device < 0) {  // host-only context: packing and index maps, no device residency
+        c->host_only = true;
+        g_err.clear();
+        *out = c;
+        return PJ_OK;
+    }
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        free_ctx(c);
+        return cuda_fail(e, "cudaSetDevice");
+    }
+    auto up = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
+        cudaError_t r = cudaMalloc(dst, bytes ? bytes : 16);
+        if (r) return r;
+        return bytes ? cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
+    };
+    cudaDeviceProp prop;
+    if ((e = cudaGetDeviceProperties(&prop, device)) ||
+        (e = up((void**)&c->d_posexp, posexp.data(), posexp.size() * 2)) ||
+        (e = up((void**)&c->d_posexp32, posexp32.data(), posexp32.size() * 4)) ||
+        (e = up((void**)&c->d_posexpF, posexpF.data(), posexpF.size() * 2)) ||
+        (e = up((void**)&c->d_coef[0], cd.data(), cd.size() * 8)) ||
+        (e = up((void**)&c->d_coef[1], cdd.data(), cdd.size() * 8)) ||
+        (e = up((void**)&c->d_coefT, cddT.data(), cddT.size() * 8)) ||
+        (e = up((void**)&c->d_gm_off, c->gm_off.data(), c->gm_off.size() * 4)) ||
+        (e = up((void**)&c->d_gm_ent, c->gm_ent.data(), c->gm_ent.size() * 2)) ||
+        (e = up((void**)&c->d_colq, colq.data(), colq.size() * 4)) ||
+        (e = up((void**)&c->d_sch, c->sch.data(), c->sch.size() * 4)) ||
+        (e = up((void**)&c->d_seg, c->seg.data(), c->seg.size() * 4)) ||
+        (e = up((void**)&c->d_segcode, c->segcode.data(), c->segcode.size() * 2)) ||
+        (e = up((void**)&c->d_segq, c->segq.data(), c->segq.size() * 4)) ||
+        (c->ragged && ((e = up((void**)&c->d_row_off, c->row_off.data(), c->row_off.size() * 4)) ||
+                       (e = up((void**)&c->d_row_chunk, c->row_chunk.data(), c->row_chunk.size() * 4)) ||
+                       (e = up((void**)&c->d_term_k, hp.term_k.data(), hp.term_k.size() * 2)))) ||
+        (e = cudaMalloc((void**)&c->d_flag, 2 * sizeof(int))) || (e = cudaMemset(c->d_flag, 0, 2 * sizeof(int)))) {
+        free_ctx(c);
+        cudaSetDevice(prev);
+        return cuda_fail(e, "pj_ctx_create: device upload");
+    }
+    for (int i = 0; i < pj_ctx::kHostStreams && !e; ++i) {
+        e = cudaStreamCreateWithFlags(&c->hstream[i], cudaStreamNonBlocking);
+        if (!e) e = cudaEventCreateWithFlags(&c->hdone[i], cudaEventDisableTiming);
+    }
+    if (e) {
+        free_ctx(c);
+        cudaSetDevice(prev);
+        return cuda_fail(e, "pj_ctx_create: streams");
+    }
+    c->sms = prop.multiProcessorCount;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
+    e = pjb::set_smem_attr(c->smem_optin);
+    if (e) {
+        free_ctx(c);
+        cudaSetDevice(prev);
+        return cuda_fail(e, "pj_ctx_create: smem attribute");
+    }
+    for (int md = 0; md < kModes; ++md) {
+        rc = choose_launch(c, md);
+        if (rc) {
+            free_ctx(c);
+            cudaSetDevice(prev);
+            return rc;
+        }
+    }
+    cudaSetDevice(prev);
+    g_err.clear();
+    *out = c;
+    return PJ_OK;
 }
 
 static int ctx_create_impl(const pj_system_desc* sys, int device, int options, pj_ctx** out) {
@@ -1023,73 +1128,209 @@ static int ctx_create_impl(const pj_system_desc* sys, int device, int options, p
         }
     }
 
-    if (device < 0) {  // host-only context: packing and index maps, no device residency
-        c->host_only = true;
-        g_err.clear();
-        *out = c;
-        return PJ_OK;
+    HostPack hp;
+    hp.posexp.swap(posexp);
+    hp.posexp32.swap(posexp32);
+    hp.posexpF.swap(posexpF);
+    hp.cd.swap(cd);
+    hp.cdd.swap(cdd);
+    hp.cddT.swap(cddT);
+    hp.colq.swap(colq);
+    return ctx_upload(c, device, hp, out);
+}
+
+// ------------------------------------------------------------------ ragged systems
+// validate_system's per-term rules and wording (ref src/system.cpp:21-64) over a CSR shape: the
+// offsets are checked first (nothing past them is indexed when they are malformed).
+static std::vector<Violation> validate_ragged(const pj_ragged_desc& S) {
+    std::vector<Violation> v;
+    auto flag = [&](int p, int g, const char* r) { v.push_back({p, g, r}); };
+    if (S.n < 1) flag(-1, -1, "n must be at least 1");
+    if (S.d < 1) flag(-1, -1, "d must be at least 1");
+    if (S.d > 255) flag(-1, -1, "d exceeds 255");
+    if (S.n < 1) return v;
+    if (!S.row_off || !S.term_off) {
+        flag(-1, -1, "missing row or term offsets");
+        return v;
     }
-    int prev = 0;
-    cudaGetDevice(&prev);
-    cudaError_t e = cudaSetDevice(device);
-    if (e != cudaSuccess) {
-        free_ctx(c);
-        return cuda_fail(e, "cudaSetDevice");
+    if (S.row_off[0] != 0) {
+        flag(-1, -1, "row offsets must start at 0");
+        return v;
     }
-    auto up = [&](void** dst, const void* src, size_t bytes) -> cudaError_t {
-        cudaError_t r = cudaMalloc(dst, bytes ? bytes : 16);
-        if (r) return r;
-        return bytes ? cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice) : cudaSuccess;
-    };
-    cudaDeviceProp prop;
-    if ((e = cudaGetDeviceProperties(&prop, device)) ||
-        (e = up((void**)&c->d_posexp, posexp.data(), posexp.size() * 2)) ||
-        (e = up((void**)&c->d_posexp32, posexp32.data(), posexp32.size() * 4)) ||
-        (e = up((void**)&c->d_posexpF, posexpF.data(), posexpF.size() * 2)) ||
-        (e = up((void**)&c->d_coef[0], cd.data(), cd.size() * 8)) ||
-        (e = up((void**)&c->d_coef[1], cdd.data(), cdd.size() * 8)) ||
-        (e = up((void**)&c->d_coefT, cddT.data(), cddT.size() * 8)) ||
-        (e = up((void**)&c->d_gm_off, c->gm_off.data(), c->gm_off.size() * 4)) ||
-        (e = up((void**)&c->d_gm_ent, c->gm_ent.data(), c->gm_ent.size() * 2)) ||
-        (e = up((void**)&c->d_colq, colq.data(), colq.size() * 4)) ||
-        (e = up((void**)&c->d_sch, c->sch.data(), c->sch.size() * 4)) ||
-        (e = up((void**)&c->d_seg, c->seg.data(), c->seg.size() * 4)) ||
-        (e = up((void**)&c->d_segcode, c->segcode.data(), c->segcode.size() * 2)) ||
-        (e = up((void**)&c->d_segq, c->segq.data(), c->segq.size() * 4)) ||
-        (e = cudaMalloc((void**)&c->d_flag, 2 * sizeof(int))) || (e = cudaMemset(c->d_flag, 0, 2 * sizeof(int)))) {
-        free_ctx(c);
-        cudaSetDevice(prev);
-        return cuda_fail(e, "pj_ctx_create: device upload");
-    }
-    for (int i = 0; i < pj_ctx::kHostStreams && !e; ++i) {
-        e = cudaStreamCreateWithFlags(&c->hstream[i], cudaStreamNonBlocking);
-        if (!e) e = cudaEventCreateWithFlags(&c->hdone[i], cudaEventDisableTiming);
-    }
-    if (e) {
-        free_ctx(c);
-        cudaSetDevice(prev);
-        return cuda_fail(e, "pj_ctx_create: streams");
-    }
-    c->sms = prop.multiProcessorCount;
-    c->smem_optin = prop.sharedMemPerBlockOptin;
-    e = pjb::set_smem_attr(c->smem_optin);
-    if (e) {
-        free_ctx(c);
-        cudaSetDevice(prev);
-        return cuda_fail(e, "pj_ctx_create: smem attribute");
-    }
-    for (int md = 0; md < kModes; ++md) {
-        rc = choose_launch(c, md);
-        if (rc) {
-            free_ctx(c);
-            cudaSetDevice(prev);
-            return rc;
+    bool shape_ok = true;
+    for (int p = 0; p < S.n; ++p) {
+        if (S.row_off[p + 1] < S.row_off[p]) {
+            flag(p, -1, "row offsets decrease");
+            shape_ok = false;
+        } else if (S.row_off[p + 1] == S.row_off[p]) {
+            flag(p, -1, "m must be at least 1");
         }
     }
-    cudaSetDevice(prev);
+    if (!shape_ok) return v;
+    const int64_t T = S.row_off[S.n];
+    if (S.term_off[0] != 0) {
+        flag(-1, -1, "term offsets must start at 0");
+        return v;
+    }
+    for (int p = 0; p < S.n; ++p)
+        for (int64_t t = S.row_off[p]; t < S.row_off[p + 1]; ++t)
+            if (S.term_off[t + 1] < S.term_off[t]) {
+                flag(p, int(t - S.row_off[p]), "term offsets decrease");
+                shape_ok = false;
+            }
+    if (!shape_ok) return v;
+    if (T > 0 && (!S.positions || !S.exponents || !S.coeffs)) {
+        flag(-1, -1, "missing term arrays");
+        return v;
+    }
+    for (int p = 0; p < S.n; ++p)
+        for (int64_t t = S.row_off[p]; t < S.row_off[p + 1]; ++t) {
+            const int g = int(t - S.row_off[p]);
+            const double* C = S.coeffs + 4 * t;
+            if (!std::isfinite(C[0]) || !std::isfinite(C[1]) || !std::isfinite(C[2]) || !std::isfinite(C[3]))
+                flag(p, g, "non-finite coefficient");
+            if (C[0] == 0.0 && C[1] == 0.0 && C[2] == 0.0 && C[3] == 0.0) flag(p, g, "zero coefficient");
+            const int kt = S.term_off[t + 1] - S.term_off[t];
+            if (kt < 1) flag(p, g, "k must be at least 1");
+            if (kt > S.n) flag(p, g, "k exceeds n");
+            const int32_t* P = S.positions + S.term_off[t];
+            const int32_t* E = S.exponents + S.term_off[t];
+            for (int j = 0; j < kt; ++j) {
+                if (P[j] < 0 || P[j] >= S.n) flag(p, g, "variable index out of range [0,n-1]");
+                if (j > 0 && P[j] <= P[j - 1]) flag(p, g, "positions not strictly increasing");
+                if (E[j] < 1 || E[j] > S.d) flag(p, g, "exponent out of range [1,d]");
+            }
+        }
+    return v;
+}
+
+int pj_validate_ragged(const pj_ragged_desc* sys, char* msg, size_t cap) {
+    if (!sys) return fail(-1, "null system descriptor");
+    auto v = validate_ragged(*sys);
+    if (msg && cap) {
+        std::string s = v.empty() ? "" : v.front().describe();
+        std::strncpy(msg, s.c_str(), cap - 1);
+        msg[cap - 1] = 0;
+    }
     g_err.clear();
-    *out = c;
-    return PJ_OK;
+    return int(v.size());
+}
+
+// Packing of a ragged system for the generic kernel (RAG = true): posexp rows of stride
+// kp = round8(max k) per term; coefficient planes [(k_max + 1)][W][T]: block j < k_t = a_j * c
+// (rounded in double like ref src/packing.cpp:47, exact in dd), block k_max = c (unused blocks 0);
+// gather map per (row chunk, column) over the global chunk index row_chunk[p] + g/32, ascending g.
+static int ctx_create_ragged_impl(const pj_ragged_desc* sys, int device, int options, pj_ctx** out) {
+    if (!out) return fail(PJ_EINVAL, "null output pointer");
+    *out = nullptr;
+    if (options & ~PJ_CTX_WIDE) return fail(PJ_EINVAL, "unknown context option");
+    if (!sys) return fail(PJ_EINVAL, "null system descriptor");
+    {
+        auto v = validate_ragged(*sys);
+        if (!v.empty()) return fail(PJ_EINVAL, "build_layout: invalid system: " + v.front().describe());
+    }
+    const bool wide_opt = options & PJ_CTX_WIDE;
+    if (!wide_opt && sys->n > 256) return fail(PJ_EINVAL, "build_layout: n > 256 does not fit the byte encoding");
+    if (wide_opt && sys->n > kWideMaxN) return fail(PJ_EINVAL, "build_layout: n exceeds the wide encoding (65535)");
+    const int n = sys->n;
+    const int64_t T = sys->row_off[n];
+    int kmax = 0, mmax = 0;
+    for (int64_t t = 0; t < T; ++t) kmax = std::max(kmax, sys->term_off[t + 1] - sys->term_off[t]);
+    for (int p = 0; p < n; ++p) mmax = std::max(mmax, sys->row_off[p + 1] - sys->row_off[p]);
+    if (kmax > 2046) return fail(PJ_EINVAL, "build_layout: k exceeds the wide encoding (2046)");
+    if (T > (int64_t(1) << 31) / (kmax + 1) / 4) return fail(PJ_EINVAL, "build_layout: too many terms");
+    pj_ctx* c = new pj_ctx();
+    c->ragged = true;
+    c->wide = wide_opt && n > 256;
+    c->device = device;
+    c->n = n;
+    c->d = sys->d;
+    c->m = mmax;
+    c->k = kmax;
+    c->kp = (kmax + 7) / 8 * 8;
+    c->chunks = (mmax + 31) / 32;
+    c->nterms = T;
+    c->row_off.assign(sys->row_off, sys->row_off + n + 1);
+    c->term_off.assign(sys->term_off, sys->term_off + T + 1);
+    c->row_chunk.assign(n + 1, 0);
+    for (int p = 0; p < n; ++p) c->row_chunk[p + 1] = c->row_chunk[p] + (c->row_off[p + 1] - c->row_off[p] + 31) / 32;
+    const size_t nslots = size_t(c->term_off[T]);
+    c->pos.assign(sys->positions, sys->positions + nslots);
+    c->exps.assign(sys->exponents, sys->exponents + nslots);
+    c->c_hi.resize(2 * size_t(T));
+    HostPack hp;
+    hp.term_k.resize(T);
+    if (c->wide)
+        hp.posexp32.assign(size_t(T) * c->kp, 0);
+    else
+        hp.posexp.assign(size_t(T) * c->kp, 0);
+    const size_t K1 = size_t(kmax) + 1, TT = size_t(T);
+    hp.cd.assign(K1 * 2 * TT, 0.0);
+    hp.cdd.assign(K1 * 4 * TT, 0.0);
+    for (size_t s = 0; s < TT; ++s) {
+        const int kt = c->term_off[s + 1] - c->term_off[s];
+        const int32_t* P = c->pos.data() + c->term_off[s];
+        const int32_t* E = c->exps.data() + c->term_off[s];
+        hp.term_k[s] = uint16_t(kt);
+        const double* C = sys->coeffs + 4 * s;
+        c->c_hi[2 * s] = C[0];
+        c->c_hi[2 * s + 1] = C[2];
+        for (int j = 0; j < kt; ++j) {
+            if (c->wide)
+                hp.posexp32[s * c->kp + j] = uint32_t(P[j]) | (uint32_t(E[j] - 1) << 16);
+            else
+                hp.posexp[s * c->kp + j] = uint16_t(P[j] | ((E[j] - 1) << 8));
+            const double a = double(E[j]);
+            hp.cd[(size_t(j) * 2 + 0) * TT + s] = a * C[0];
+            hp.cd[(size_t(j) * 2 + 1) * TT + s] = a * C[2];
+            double h, l;
+            dd_mul_small(C[0], C[1], a, &h, &l);
+            hp.cdd[(size_t(j) * 4 + 0) * TT + s] = h;
+            hp.cdd[(size_t(j) * 4 + 1) * TT + s] = l;
+            dd_mul_small(C[2], C[3], a, &h, &l);
+            hp.cdd[(size_t(j) * 4 + 2) * TT + s] = h;
+            hp.cdd[(size_t(j) * 4 + 3) * TT + s] = l;
+        }
+        hp.cd[(size_t(kmax) * 2 + 0) * TT + s] = C[0];
+        hp.cd[(size_t(kmax) * 2 + 1) * TT + s] = C[2];
+        for (int q = 0; q < 4; ++q) hp.cdd[(size_t(kmax) * 4 + q) * TT + s] = C[q];
+    }
+    // gather map: lists (global chunk, column), ascending g within the row
+    const size_t nlists = size_t(c->row_chunk[n]) * n;
+    std::vector<int> cnt(nlists + 1, 0);
+    for (int p = 0; p < n; ++p)
+        for (int64_t s = c->row_off[p]; s < c->row_off[p + 1]; ++s) {
+            const int g = int(s - c->row_off[p]);
+            for (int32_t q = c->term_off[s]; q < c->term_off[s + 1]; ++q)
+                cnt[size_t(c->row_chunk[p] + g / 32) * n + c->pos[q]]++;
+        }
+    c->gm_off.assign(nlists + 1, 0);
+    for (size_t i = 0; i < nlists; ++i) c->gm_off[i + 1] = c->gm_off[i] + cnt[i];
+    c->gm_ent.assign(c->gm_off.back(), 0);
+    {
+        std::vector<int> fill(c->gm_off.begin(), c->gm_off.end() - 1);
+        for (int p = 0; p < n; ++p)
+            for (int64_t s = c->row_off[p]; s < c->row_off[p + 1]; ++s) {
+                const int g = int(s - c->row_off[p]);
+                for (int32_t q = c->term_off[s]; q < c->term_off[s + 1]; ++q) {
+                    const size_t li = size_t(c->row_chunk[p] + g / 32) * n + c->pos[q];
+                    c->gm_ent[fill[li]++] = uint16_t((q - c->term_off[s]) * 32 + (g & 31));
+                }
+            }
+    }
+    return ctx_upload(c, device, hp, out);
+}
+
+int pj_ctx_create_ragged(const pj_ragged_desc* sys, int device, int options, pj_ctx** out) {
+    try {
+        return ctx_create_ragged_impl(sys, device, options, out);
+    } catch (const std::bad_alloc&) {
+        if (out) *out = nullptr;
+        return fail(PJ_ENOMEM, "pj_ctx_create_ragged: host allocation failed");
+    } catch (const std::exception& ex) {
+        if (out) *out = nullptr;
+        return fail(PJ_ENOMEM, std::string("pj_ctx_create_ragged: ") + ex.what());
+    }
 }
 
 void pj_ctx_destroy(pj_ctx* ctx) { free_ctx(ctx); }
@@ -1121,7 +1362,10 @@ int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, d
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != ctx->device) PJ_CUDA(cudaSetDevice(ctx->device));
-    const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
+    // the global-scratch slab is shared by the modes and reallocated when a later mode (or a
+    // pj_set_launch) needs more: read the current pointer, never the one stored at planning time
+    pjb::LaunchCfg L = ctx->mode[mode_of(flags)].cfg;
+    if (L.gscratch) L.gscratch = ctx->d_scratch;
     if (flags & PJ_VALIDATE) {
         // reject before any output is written, like ref src/engine.cpp:183-188: check the batch on
         // `stream`, read the verdict back (the one synchronisation of this mode)
@@ -1249,7 +1493,7 @@ int pj_layout_info(const pj_ctx* ctx, int32_t* n, int32_t* m, int32_t* k, int32_
     if (m) *m = ctx->m;
     if (k) *k = ctx->k;
     if (d) *d = ctx->d;
-    if (footprint) *footprint = 2 * int64_t(ctx->n) * ctx->m * ctx->k;
+    if (footprint) *footprint = ctx->ragged ? 2 * int64_t(ctx->term_off.back()) : 2 * int64_t(ctx->n) * ctx->m * ctx->k;
     g_err.clear();
     return PJ_OK;
 }
@@ -1270,6 +1514,7 @@ int pj_mons_slot(int64_t s, int kind, int var, int n, int m, int64_t* slot) {
 
 int pj_slot_targets(const pj_ctx* ctx, int64_t s, int64_t* targets) {
     if (!ctx) return fail(PJ_EINVAL, "null context");
+    if (ctx->ragged) return fail(PJ_EINVAL, "slot_targets: the Mons slot map is defined for uniform systems only");
     for (int j = 0; j < ctx->k; ++j) {
         int rc = pj_mons_slot(s, 1, s >= 0 && s < int64_t(ctx->n) * ctx->m ? ctx->pos[s * ctx->k + j] : 0,
                               ctx->n, ctx->m, targets + j);
@@ -1280,6 +1525,7 @@ int pj_slot_targets(const pj_ctx* ctx, int64_t s, int64_t* targets) {
 
 int64_t pj_zero_mask(const pj_ctx* ctx, int64_t* mask, int64_t cap) {
     if (!ctx) return fail(-1, "null context");
+    if (ctx->ragged) return fail(-1, "zero_mask: the Mons buffer is defined for uniform systems only");
     // Regenerated from the device gather map: a Mons slot is claimed iff it is a value slot or
     // its (p, v, g) appears in the (p, chunk(g), v) list. Everything else is the zero mask.
     const int64_t n = ctx->n, m = ctx->m, C = ctx->chunks, stride = n * n + n;
@@ -1308,6 +1554,7 @@ int64_t pj_zero_mask(const pj_ctx* ctx, int64_t* mask, int64_t cap) {
 int pj_layout_export(const pj_ctx* ctx, uint8_t* positions, uint8_t* exponents, double* coeffs) {
     if (!ctx) return fail(PJ_EINVAL, "null context");
     if (ctx->n > 256) return fail(PJ_EINVAL, "layout: n > 256 has no byte encoding (wide context)");
+    if (ctx->ragged) return fail(PJ_EINVAL, "layout: PackedLayout is defined for uniform systems only");
     const size_t nm = size_t(ctx->n) * ctx->m, k = size_t(ctx->k);
     // ref src/packing.cpp:40-49: positions / exponents-minus-one bytes in S_m order; coefficient
     // blocks derivative-major, block j < k = a_j * c rounded per component in double, block k = c.
@@ -1338,8 +1585,10 @@ int64_t pj_structural_zeros(const pj_ctx* ctx, uint8_t* mask) {
     for (int p = 0; p < n; ++p)
         for (int v = 0; v < n; ++v) {
             bool any = false;
-            for (int c = 0; c < C && !any; ++c) {
-                const size_t li = (size_t(p) * C + c) * n + v;
+            const int cb = ctx->ragged ? ctx->row_chunk[p] : p * C;
+            const int nch = ctx->ragged ? ctx->row_chunk[p + 1] - cb : C;
+            for (int c = 0; c < nch && !any; ++c) {
+                const size_t li = (size_t(cb) + c) * n + v;
                 any = ctx->gm_off[li + 1] > ctx->gm_off[li];
             }
             if (mask) mask[size_t(p) * n + v] = any ? 0 : 1;
@@ -1352,6 +1601,7 @@ int64_t pj_structural_zeros(const pj_ctx* ctx, uint8_t* mask) {
 int pj_debug_corrupt_coeff(pj_ctx* ctx, int64_t s, double factor) {
     if (!ctx) return fail(PJ_EINVAL, "null context");
     if (ctx->host_only) return fail(PJ_EINVAL, "host-only context");
+    if (ctx->ragged) return fail(PJ_EINVAL, "corrupt_coeff: uniform systems only");
     const int64_t nm = int64_t(ctx->n) * ctx->m;
     if (s < 0 || s >= nm) return fail(PJ_ERANGE, "corrupt_coeff: monomial index " + std::to_string(s));
     DeviceGuard dg;
@@ -1379,6 +1629,23 @@ int pj_mult_counts(const pj_ctx* ctx, int64_t evals, uint64_t* counts) {
     if (!ctx || !counts) return fail(PJ_EINVAL, "null argument");
     const uint64_t n = ctx->n, nm = uint64_t(ctx->n) * ctx->m, k = ctx->k, d = ctx->d;
     const uint64_t sp = k >= 3 ? 3 * k - 6 : 0;
+    if (ctx->ragged) {  // the closed form per term, summed (SPEC.md:477 with k -> k_t)
+        uint64_t f = 0, s2 = 0, s3 = 0;
+        for (int64_t t = 0; t < ctx->nterms; ++t) {
+            const uint64_t kt = uint64_t(ctx->term_off[t + 1] - ctx->term_off[t]);
+            const uint64_t spt = kt >= 3 ? 3 * kt - 6 : 0;
+            f += kt - 1;
+            s2 += spt + 2 * kt + 2;
+            s3 += spt;
+        }
+        counts[0] = uint64_t(evals) * n * (d >= 2 ? d - 2 : 0);
+        counts[1] = uint64_t(evals) * f;
+        counts[2] = uint64_t(evals) * s2;
+        counts[3] = uint64_t(evals) * s3;
+        counts[4] = 0;
+        g_err.clear();
+        return PJ_OK;
+    }
     counts[0] = uint64_t(evals) * n * (d >= 2 ? d - 2 : 0);
     counts[1] = uint64_t(evals) * nm * (k - 1);
     counts[2] = uint64_t(evals) * nm * (sp + 2 * k + 2);
@@ -1439,6 +1706,44 @@ int pj_random_system(int n, int m, int k, int d, uint64_t seed, int32_t* positio
         coeffs[4 * s + 2] = im;
         coeffs[4 * s + 3] = 0.0;
     }
+    g_err.clear();
+    return PJ_OK;
+}
+
+int pj_random_ragged_system(int n, int m_lo, int m_hi, int k_lo, int k_hi, int d, uint64_t seed, int64_t* T,
+                            int64_t* S, int32_t* row_off, int32_t* term_off, int32_t* positions, int32_t* exponents,
+                            double* coeffs) {
+    if (n < 1) return fail(PJ_EINVAL, "random_ragged_system: n must be at least 1");
+    if (m_lo < 1 || m_hi < m_lo) return fail(PJ_EINVAL, "random_ragged_system: need 1 <= m_lo <= m_hi");
+    if (k_lo < 1 || k_hi < k_lo || k_hi > n) return fail(PJ_EINVAL, "random_ragged_system: need 1 <= k_lo <= k_hi <= n");
+    if (d < 1 || d > 255) return fail(PJ_EINVAL, "random_ragged_system: need 1 <= d <= 255");
+    Gen r(seed);
+    std::vector<int32_t> ro(n + 1, 0), to(1, 0), ps, es;
+    std::vector<double> cs;
+    std::vector<int> idx(n);
+    for (int p = 0; p < n; ++p) ro[p + 1] = ro[p] + m_lo + int(r.below(uint64_t(m_hi - m_lo + 1)));
+    for (int32_t t = 0; t < ro[n]; ++t) {
+        const int k = k_lo + int(r.below(uint64_t(k_hi - k_lo + 1)));
+        for (int i = 0; i < n; ++i) idx[i] = i;
+        for (int j = 0; j < k; ++j) std::swap(idx[j], idx[j + int(r.below(uint64_t(n - j)))]);
+        std::sort(idx.begin(), idx.begin() + k);
+        for (int j = 0; j < k; ++j) ps.push_back(idx[j]);
+        for (int j = 0; j < k; ++j) es.push_back(1 + int(r.below(uint64_t(d))));
+        double re, im;
+        do {
+            re = r.sym();
+            im = r.sym();
+        } while (re == 0.0 && im == 0.0);
+        cs.insert(cs.end(), {re, 0.0, im, 0.0});
+        to.push_back(to.back() + k);
+    }
+    if (T) *T = ro[n];
+    if (S) *S = to.back();
+    if (row_off) std::copy(ro.begin(), ro.end(), row_off);
+    if (term_off) std::copy(to.begin(), to.end(), term_off);
+    if (positions) std::copy(ps.begin(), ps.end(), positions);
+    if (exponents) std::copy(es.begin(), es.end(), exponents);
+    if (coeffs) std::copy(cs.begin(), cs.end(), coeffs);
     g_err.clear();
     return PJ_OK;
 }

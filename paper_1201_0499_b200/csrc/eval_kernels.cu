@@ -56,7 +56,11 @@ __device__ __forceinline__ void st_pr(double* base, int e, int P, const CDD& v) 
 constexpr int kRef = 0;
 constexpr int kFast = 1;
 
-template <class T, int ORDER, bool GSCR>
+// RAG: ragged system: row p owns terms [row_off[p], row_off[p+1])
+// and stage-3 chunks [row_chunk[p], row_chunk[p+1]); term s has term_k[s] <= k variables (k = the
+// maximum). Per term the reference's stage-1/2 sequence for its own k_s; the value coefficient and
+// value staging slot sit at block k (the uniform layout's block k), derivative j at block j.
+template <class T, int ORDER, bool GSCR, bool RAG>
 __global__ void __launch_bounds__(256) eval_kernel(DevSystem S, const double* __restrict__ pts,
                                                    double* __restrict__ out, long long B, int TP,
                                                    double* __restrict__ gscratch, int* __restrict__ flag) {
@@ -64,11 +68,12 @@ __global__ void __launch_bounds__(256) eval_kernel(DevSystem S, const double* __
     constexpr int W = O::W;
     extern __shared__ __align__(16) double smem_[];
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int n = S.n, k = S.k, m = S.m, d = S.d;
+    const int n = S.n, m = S.m, d = S.d;
+    const int kv = S.k;  // value block / staging row (the maximum k of a ragged system)
     auto LD = [](const double* base, int e, int P) -> T { return ld_pr(base, e, P, static_cast<T*>(nullptr)); };
     const int D1 = d > 2 ? d - 1 : 1;  // stored powers e = 1..D1
     const int tabPt = D1 * W * n;      // doubles per point
-    const int stgW = (k + 1) * W * 32;  // staging doubles per warp
+    const int stgW = (kv + 1) * W * 32;  // staging doubles per warp
     const int accW = (n + 1) * W;      // accumulator doubles per warp
     double* base = GSCR ? gscratch + (size_t)blockIdx.x * (TP * tabPt + nw * (stgW + accW)) : smem_;
     double* tab = base;
@@ -108,11 +113,17 @@ __global__ void __launch_bounds__(256) eval_kernel(DevSystem S, const double* __
             const double* xt = tab + t * tabPt;
             double* orow = out + ((b0 + t) * nout) * W;
             T vacc = O::zero();
-            for (int c = 0; c < S.chunks; ++c) {
+            // row p: its terms [s0, s0 + mrow) and stage-3 chunks [cb, cb + nch)
+            const int s0 = RAG ? __ldg(S.row_off + p) : p * m;
+            const int mrow = RAG ? __ldg(S.row_off + p + 1) - s0 : m;
+            const int cb = RAG ? __ldg(S.row_chunk + p) : p * S.chunks;
+            const int nch = RAG ? __ldg(S.row_chunk + p + 1) - cb : S.chunks;
+            for (int c = 0; c < nch; ++c) {
                 const int g = c * 32 + lane;
                 T valterm = O::zero();
-                if (g < m) {
-                    const int s = p * m + g;
+                if (g < mrow) {
+                    const int s = s0 + g;
+                    const int k = RAG ? int(__ldg(S.term_k + s)) : S.k;  // this term's variables
                     const uint16_t* pe = S.posexp + (size_t)s * S.kp;
                     const uint32_t* pe32 = S.posexp32 + (size_t)s * S.kp;
                     const bool wide = S.posexp32 != nullptr;  // uniform across the grid
@@ -146,14 +157,14 @@ __global__ void __launch_bounds__(256) eval_kernel(DevSystem S, const double* __
                         T L0 = O::mul(O::one(), f);
                         T val = O::mul(L0, X(0));
                         st_pr(SLOT(0), lane, 32, O::mul(L0, COEF(0)));
-                        valterm = O::mul(val, COEF(1));
+                        valterm = O::mul(val, COEF(kv));
                     } else if (k == 2) {
                         const T v0 = X(0), v1 = X(1);
                         T L0 = O::mul(v1, f), L1 = O::mul(v0, f);
                         T val = O::mul(L1, v1);
                         st_pr(SLOT(0), lane, 32, O::mul(L0, COEF(0)));
                         st_pr(SLOT(1), lane, 32, O::mul(L1, COEF(1)));
-                        valterm = O::mul(val, COEF(2));
+                        valterm = O::mul(val, COEF(kv));
                     } else {
                         // forward products L[1] = v0, L[r+2] = L[r+1] * v[r+1]
                         T F = X(0);
@@ -184,15 +195,15 @@ __global__ void __launch_bounds__(256) eval_kernel(DevSystem S, const double* __
                         T Lk1 = O::mul(F, f);
                         T val = O::mul(Lk1, vlast);
                         st_pr(SLOT(k - 1), lane, 32, O::mul(Lk1, COEF(k - 1)));
-                        valterm = O::mul(val, COEF(k));
+                        valterm = O::mul(val, COEF(kv));
                     }
-                    if (ORDER == kRef) st_pr(SLOT(k), lane, 32, valterm);
+                    if (ORDER == kRef) st_pr(SLOT(kv), lane, 32, valterm);
                 }
                 __syncwarp();
                 // stage 3 (Jacobian): ascending-g ordered gather over the (row, column) map
-                const bool last = c + 1 == S.chunks;
+                const bool last = c + 1 == nch;
                 for (int v = lane; v < n; v += 32) {
-                    const int li = (p * S.chunks + c) * n + v;
+                    const int li = (cb + c) * n + v;
                     const int e0 = __ldg(S.gm_off + li), e1 = __ldg(S.gm_off + li + 1);
                     T a = c == 0 ? O::zero() : LD(acc, v, n + 1);
                     for (int e = e0; e < e1; ++e) {
@@ -207,8 +218,8 @@ __global__ void __launch_bounds__(256) eval_kernel(DevSystem S, const double* __
                 // stage 3 (value)
                 if (ORDER == kRef) {
                     if (lane == 0) {
-                        const int gl = min(32, m - c * 32);
-                        for (int gg = 0; gg < gl; ++gg) vacc = O::add(vacc, LD(stg + k * W * 32, gg, 32));
+                        const int gl = min(32, mrow - c * 32);
+                        for (int gg = 0; gg < gl; ++gg) vacc = O::add(vacc, LD(stg + kv * W * 32, gg, 32));
                     }
                 } else {
                     T r = valterm;
@@ -224,10 +235,10 @@ __global__ void __launch_bounds__(256) eval_kernel(DevSystem S, const double* __
     }
 }
 
-template <class T, int ORDER, bool GSCR>
+template <class T, int ORDER, bool GSCR, bool RAG>
 static cudaError_t launch_one(const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
                               cudaStream_t st) {
-    auto kern = eval_kernel<T, ORDER, GSCR>;
+    auto kern = eval_kernel<T, ORDER, GSCR, RAG>;
     if (!GSCR && L.smem_bytes > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_limit((const void*)kern));
         if (e != cudaSuccess) return e;
@@ -236,27 +247,33 @@ static cudaError_t launch_one(const LaunchCfg& L, const DevSystem& S, const doub
     return cudaGetLastError();
 }
 
-cudaError_t launch_eval(int prec, int order, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out,
-                        long long B, cudaStream_t st) {
-    const bool g = L.gscratch != nullptr;
-    if (prec == 1) {
-        if (order == kRef) return g ? launch_one<CD, kRef, true>(L, S, pts, out, B, st) : launch_one<CD, kRef, false>(L, S, pts, out, B, st);
-        return g ? launch_one<CD, kFast, true>(L, S, pts, out, B, st) : launch_one<CD, kFast, false>(L, S, pts, out, B, st);
-    }
-    if (order == kRef) return g ? launch_one<CDD, kRef, true>(L, S, pts, out, B, st) : launch_one<CDD, kRef, false>(L, S, pts, out, B, st);
-    return g ? launch_one<CDD, kFast, true>(L, S, pts, out, B, st) : launch_one<CDD, kFast, false>(L, S, pts, out, B, st);
+template <class T, int ORDER>
+static cudaError_t launch_to(const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
+                             cudaStream_t st) {
+    const bool g = L.gscratch != nullptr, r = S.row_off != nullptr;
+    if (r) return g ? launch_one<T, ORDER, true, true>(L, S, pts, out, B, st) : launch_one<T, ORDER, false, true>(L, S, pts, out, B, st);
+    return g ? launch_one<T, ORDER, true, false>(L, S, pts, out, B, st) : launch_one<T, ORDER, false, false>(L, S, pts, out, B, st);
 }
 
-int max_blocks_per_sm(int prec, int order, int threads, size_t smem) {
+cudaError_t launch_eval(int prec, int order, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out,
+                        long long B, cudaStream_t st) {
+    if (prec == 1) return order == kRef ? launch_to<CD, kRef>(L, S, pts, out, B, st) : launch_to<CD, kFast>(L, S, pts, out, B, st);
+    return order == kRef ? launch_to<CDD, kRef>(L, S, pts, out, B, st) : launch_to<CDD, kFast>(L, S, pts, out, B, st);
+}
+
+template <class T, int ORDER, bool RAG>
+static int occ_one(int threads, size_t smem) {
     int nb = 0;
-    cudaError_t e;
-    if (prec == 1)
-        e = order == kRef ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_kernel<CD, kRef, false>, threads, smem)
-                          : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_kernel<CD, kFast, false>, threads, smem);
-    else
-        e = order == kRef ? cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_kernel<CDD, kRef, false>, threads, smem)
-                          : cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_kernel<CDD, kFast, false>, threads, smem);
-    return e == cudaSuccess ? nb : 0;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, eval_kernel<T, ORDER, false, RAG>, threads, smem) == cudaSuccess ? nb : 0;
+}
+
+int max_blocks_per_sm(int prec, int order, int threads, size_t smem, bool ragged) {
+    if (ragged) {
+        if (prec == 1) return order == kRef ? occ_one<CD, kRef, true>(threads, smem) : occ_one<CD, kFast, true>(threads, smem);
+        return order == kRef ? occ_one<CDD, kRef, true>(threads, smem) : occ_one<CDD, kFast, true>(threads, smem);
+    }
+    if (prec == 1) return order == kRef ? occ_one<CD, kRef, false>(threads, smem) : occ_one<CD, kFast, false>(threads, smem);
+    return order == kRef ? occ_one<CDD, kRef, false>(threads, smem) : occ_one<CDD, kFast, false>(threads, smem);
 }
 
 int dyn_smem_limit(const void* f) {
@@ -289,16 +306,17 @@ cudaError_t launch_check_finite(const double* pts, long long doubles, int* flag,
 }
 
 // Prime the dynamic-smem attribute so the occupancy query sees the opt-in limit.
+template <class T, int ORDER>
+static cudaError_t set_attr_pair(int b) {
+    cudaError_t e = cudaFuncSetAttribute(eval_kernel<T, ORDER, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    if (e) return e;
+    return cudaFuncSetAttribute(eval_kernel<T, ORDER, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+}
 cudaError_t set_smem_attr(size_t bytes) {
-    cudaError_t e = cudaSuccess;
-    int b = (int)bytes;
-    e = cudaFuncSetAttribute(eval_kernel<CD, kRef, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    if (e) return e;
-    e = cudaFuncSetAttribute(eval_kernel<CD, kFast, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    if (e) return e;
-    e = cudaFuncSetAttribute(eval_kernel<CDD, kRef, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
-    if (e) return e;
-    return cudaFuncSetAttribute(eval_kernel<CDD, kFast, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, b);
+    const int b = (int)bytes;
+    cudaError_t e;
+    if ((e = set_attr_pair<CD, kRef>(b)) || (e = set_attr_pair<CD, kFast>(b)) || (e = set_attr_pair<CDD, kRef>(b))) return e;
+    return set_attr_pair<CDD, kFast>(b);
 }
 
 }  // namespace pjb

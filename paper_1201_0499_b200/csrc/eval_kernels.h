@@ -47,6 +47,13 @@ struct DevSystem {
     // colq[(p*chunks + c)*n + i] = {first gm_ent entry, count | column << 16} (column 0 always at
     // slot 0; the grouping of columns into quarter-warps is chosen against bank conflicts)
     const int2* colq;
+    // ragged system (null for a uniform one, which uses p*m and p*chunks): the
+    // terms of row p are [row_off[p], row_off[p+1]) (s = row_off[p] + g), its stage-3 chunks
+    // [row_chunk[p], row_chunk[p+1]) (gm_off index (row_chunk[p] + c)*n + v), term s has term_k[s]
+    // variables; k above is the maximum, nm the total term count
+    const int* row_off = nullptr;
+    const int* row_chunk = nullptr;
+    const uint16_t* term_k = nullptr;
     // plain dd coefficients tiled for the fast kernel: component q of monomial
     // g = 32*chunk + lane of row p at coefT[((p*chunks + chunk)*4 + q)*32 + lane] (0 for g >= m)
     const double* coefT;
@@ -67,7 +74,7 @@ struct LaunchCfg {
 
 cudaError_t launch_eval(int prec, int order, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out,
                         long long B, cudaStream_t st);
-int max_blocks_per_sm(int prec, int order, int threads, size_t smem);
+int max_blocks_per_sm(int prec, int order, int threads, size_t smem, bool ragged);
 // sets *flag |= 1 when any of the `doubles` words at pts is non-finite (points: 16-byte aligned)
 cudaError_t launch_check_finite(const double* pts, long long doubles, int* flag, int sms, cudaStream_t st);
 cudaError_t set_smem_attr(size_t bytes);

@@ -27,7 +27,7 @@ from typing import List, Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import PJ_ORDER_FAST, PJ_ORDER_REF, PJ_PREC_D, PJ_PREC_DD, SystemDesc, check, lib
+from ._lib import PJ_ORDER_FAST, PJ_ORDER_REF, PJ_PREC_D, PJ_PREC_DD, RaggedDesc, SystemDesc, check, lib
 
 
 # --------------------------------------------------------------------------- system model
@@ -142,6 +142,110 @@ def random_system(n: int, m: int, k: int, d: int, seed: int) -> PolynomialSystem
     co = np.empty((nm, 4), np.float64)
     check(lib().pj_random_system(n, m, k, d, seed, pos.ctypes.data, exps.ctypes.data, co.ctypes.data))
     return PolynomialSystem(n, m, k, d, pos, exps, co)
+
+
+# --------------------------------------------------------------------------- ragged systems (f4)
+@dataclass
+class RaggedSystem:
+    """Non-uniform m and k (include/polyjac_b200.h pj_ragged_desc): polynomial p
+    owns terms [row_off[p], row_off[p+1]), term t owns positions/exponents [term_off[t],
+    term_off[t+1]); coeffs float64 [T, 4] = (re_hi, re_lo, im_hi, im_lo). Per-term rules as
+    validate_system (ref src/system.cpp:21-64)."""
+    n: int
+    d: int
+    row_off: np.ndarray
+    term_off: np.ndarray
+    positions: np.ndarray
+    exponents: np.ndarray
+    coeffs: np.ndarray
+
+    @property
+    def term_count(self) -> int:
+        return int(self.row_off[self.n])
+
+    def m_of(self, p: int) -> int:
+        return int(self.row_off[p + 1] - self.row_off[p])
+
+    def k_of(self, t: int) -> int:
+        return int(self.term_off[t + 1] - self.term_off[t])
+
+    def term(self, p: int, g: int) -> Term:
+        t = int(self.row_off[p]) + g
+        a, b = int(self.term_off[t]), int(self.term_off[t + 1])
+        c = self.coeffs[t]
+        return Term(complex(c[0] + c[1], c[2] + c[3]),
+                    MonomialSupport([int(v) for v in self.positions[a:b]], [int(v) for v in self.exponents[a:b]]))
+
+    @staticmethod
+    def from_uniform(sys: PolynomialSystem) -> "RaggedSystem":
+        """The same uniform system in ragged form (evaluates bit-identically)."""
+        nm = sys.n * sys.m
+        return RaggedSystem(sys.n, sys.d, np.arange(sys.n + 1, dtype=np.int32) * sys.m,
+                            np.arange(nm + 1, dtype=np.int32) * sys.k,
+                            np.ascontiguousarray(sys.positions, np.int32).reshape(-1).copy(),
+                            np.ascontiguousarray(sys.exponents, np.int32).reshape(-1).copy(),
+                            np.ascontiguousarray(sys.coeffs, np.float64).reshape(nm, 4).copy())
+
+    @staticmethod
+    def from_polynomials(n: int, d: int, polys: Sequence[Sequence[Term]]) -> "RaggedSystem":
+        """From n lists of Terms (each term with its own support size)."""
+        ro, to, ps, es, cs = [0], [0], [], [], []
+        for terms in polys:
+            for t in terms:
+                ps.extend(t.support.positions)
+                es.extend(t.support.exponents)
+                to.append(to[-1] + len(t.support.positions))
+                c = complex(t.coeff)
+                cs.append((c.real, 0.0, c.imag, 0.0))
+            ro.append(ro[-1] + len(terms))
+        return RaggedSystem(n, d, np.array(ro, np.int32), np.array(to, np.int32), np.array(ps, np.int32),
+                            np.array(es, np.int32), np.array(cs, np.float64).reshape(-1, 4))
+
+    def as_dict(self) -> dict:
+        """Array dict for the oracle (tests only)."""
+        return dict(n=self.n, d=self.d, row_off=self.row_off, term_off=self.term_off, pos=self.positions,
+                    exps=self.exponents, coeffs=self.coeffs)
+
+    def _desc(self):
+        arrs = (np.ascontiguousarray(self.row_off, np.int32), np.ascontiguousarray(self.term_off, np.int32),
+                np.ascontiguousarray(self.positions, np.int32), np.ascontiguousarray(self.exponents, np.int32),
+                np.ascontiguousarray(self.coeffs, np.float64))
+        if arrs[0].size != self.n + 1 or arrs[1].size < 1:
+            raise ValueError("ragged system: row_off needs n + 1 entries and term_off at least one")
+        T = int(arrs[0][-1])
+        if arrs[1].size != T + 1 or arrs[2].size < int(arrs[1][-1]) or arrs[3].size < int(arrs[1][-1]) \
+                or arrs[4].size != 4 * T:
+            raise ValueError("ragged system: array sizes do not match row_off / term_off")
+        desc = RaggedDesc(self.n, self.d, *(a.ctypes.data for a in arrs))
+        return desc, arrs
+
+
+def validate_ragged_system(sys: RaggedSystem) -> ValidationReport:
+    desc, keep = sys._desc()
+    buf = ctypes.create_string_buffer(512)
+    nv = lib().pj_validate_ragged(ctypes.byref(desc), buf, 512)
+    rep = ValidationReport()
+    if nv > 0:
+        rep.violations.append(Violation(-1, -1, buf.value.decode()))
+        rep.violations.extend(Violation(-1, -1, "") for _ in range(nv - 1))
+    return rep
+
+
+def random_ragged_system(n: int, m_range, k_range, d: int, seed: int) -> RaggedSystem:
+    """m_p uniform in m_range = (lo, hi) per polynomial, k_t uniform in k_range per term, then the
+    reference generator's per-term draws (pj_random_ragged_system)."""
+    T, S = ctypes.c_int64(), ctypes.c_int64()
+    L = lib()
+    args = (n, int(m_range[0]), int(m_range[1]), int(k_range[0]), int(k_range[1]), d, seed)
+    check(L.pj_random_ragged_system(*args, ctypes.byref(T), ctypes.byref(S), None, None, None, None, None))
+    ro = np.empty(n + 1, np.int32)
+    to = np.empty(T.value + 1, np.int32)
+    ps = np.empty(max(S.value, 1), np.int32)
+    es = np.empty(max(S.value, 1), np.int32)
+    co = np.empty((T.value, 4), np.float64)
+    check(L.pj_random_ragged_system(*args, None, None, ro.ctypes.data, to.ctypes.data, ps.ctypes.data,
+                                    es.ctypes.data, co.ctypes.data))
+    return RaggedSystem(n, d, ro, to, ps[:S.value], es[:S.value], co)
 
 
 def random_points(n: int, count: int, seed: int) -> np.ndarray:
@@ -310,20 +414,32 @@ class EvaluationContext:
     Like the reference, one context must not serve concurrent evaluate calls; use one per
     thread (or per device / stream)."""
 
-    def __init__(self, sys: PolynomialSystem, grid: GridConfig | None = None, device: int = 0, wide: bool = False):
-        """wide=True lifts the reference's n <= 256 byte-encoding cap (pj_ctx_create_ex, PJ_CTX_WIDE)."""
+    def __init__(self, sys: PolynomialSystem | RaggedSystem, grid: GridConfig | None = None, device: int = 0,
+                 wide: bool = False):
+        """wide=True lifts the reference's n <= 256 byte-encoding cap (pj_ctx_create_ex, PJ_CTX_WIDE).
+        A RaggedSystem (non-uniform m / k, SURVEY.md §8f f4) goes through pj_ctx_create_ragged;
+        self.m / self.k are then the maxima."""
         grid = grid or GridConfig()
         if grid.block_size < 1:
             raise ValueError("block size must be >= 1")
         if grid.workers < 0:
             raise ValueError("workers must be >= 0")
         self.grid_ = GridConfig(grid.block_size, grid.workers if grid.workers > 0 else 1)
-        self.n, self.m, self.k, self.d = sys.n, sys.m, sys.k, sys.d
         self.device = device
+        self.ragged = isinstance(sys, RaggedSystem)
         desc, keep = sys._desc()
         h = ctypes.c_void_p()
-        check(lib().pj_ctx_create_ex(ctypes.byref(desc), device, _lib.PJ_CTX_WIDE if wide else 0, ctypes.byref(h)))
+        opts = _lib.PJ_CTX_WIDE if wide else 0
+        if self.ragged:
+            check(lib().pj_ctx_create_ragged(ctypes.byref(desc), device, opts, ctypes.byref(h)))
+        else:
+            check(lib().pj_ctx_create_ex(ctypes.byref(desc), device, opts, ctypes.byref(h)))
         self._h = h
+        if self.ragged:
+            info = self.layout_info()
+            self.n, self.m, self.k, self.d = info["n"], info["m"], info["k"], info["d"]
+        else:
+            self.n, self.m, self.k, self.d = sys.n, sys.m, sys.k, sys.d
         self._mults = MultCounter()
         self._clean = True
         self._zeros = None
