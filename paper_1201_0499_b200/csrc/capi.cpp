@@ -206,10 +206,16 @@ void parallel_rows(int n, F&& fn) {
 // gather x from distinct bank quads (point table: 16-byte unit = position). The monomial's
 // products commute, so only rounding changes (the fast order's contract).
 // perm[g*k + j] = original index of the variable the kernel visits at step j.
-void order_variables(const int32_t* pos, int gl, int k, int p_seed, std::vector<uint8_t>& perm) {
+// exps (d <= 2, else null): the kernel's d <= 2 path reads the common factor off its suffix-product
+// chain, so every monomial's exponent-2 variables must come last; swaps stay inside a group.
+void order_variables(const int32_t* pos, const int32_t* exps, int gl, int k, int p_seed, std::vector<uint8_t>& perm) {
     perm.resize(size_t(gl) * k);
-    for (int g = 0; g < gl; ++g)
-        for (int j = 0; j < k; ++j) perm[g * k + j] = uint8_t(j);
+    for (int g = 0; g < gl; ++g) {
+        int at = 0;
+        for (int pass = 0; pass < (exps ? 2 : 1); ++pass)  // exponent-1 variables first, then exponent 2
+            for (int j = 0; j < k; ++j)
+                if (!exps || (exps[size_t(g) * k + j] == 1) == (pass == 0)) perm[g * k + at++] = uint8_t(j);
+    }
     if (k < 2) return;
     auto step_cost = [&](int qw, int j) {
         int a[8];
@@ -226,6 +232,7 @@ void order_variables(const int32_t* pos, int gl, int k, int p_seed, std::vector<
         const int a = int(r.next(uint32_t(k)));
         int b = int(r.next(uint32_t(k - 1)));
         b += b >= a;
+        if (exps && exps[size_t(g) * k + perm[g * k + a]] != exps[size_t(g) * k + perm[g * k + b]]) continue;
         const int qw = g / 8;
         const int before = step_cost(qw, a) + step_cost(qw, b);
         std::swap(perm[g * k + a], perm[g * k + b]);
@@ -967,7 +974,8 @@ static int ctx_create_impl(const pj_system_desc* sys, int device, int options, p
             for (int ch = 0; ch < C; ++ch) {
                 const int gl = std::min(32, c->m - ch * 32);
                 const size_t s0 = size_t(p) * c->m + size_t(ch) * 32;
-                order_variables(c->pos.data() + s0 * k, gl, kk, p * C + ch, perm);
+                order_variables(c->pos.data() + s0 * k, c->d <= 2 ? c->exps.data() + s0 * k : nullptr, gl, kk, p * C + ch,
+                                perm);
                 for (int g = 0; g < gl; ++g)
                     for (int j = 0; j < kk; ++j) {
                         const size_t s = s0 + g;

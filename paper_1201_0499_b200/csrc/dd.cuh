@@ -34,11 +34,32 @@ __device__ __forceinline__ CD cd_add(CD a, CD b) { return {__dadd_rn(a.re, b.re)
 struct DD {
     double hi, lo;
 };
+// Error-free sum s + e = a + b. Every variant returns s = fl(a + b) and the EXACT error e, so all
+// give identical bits (the oracle keeps Knuth's form):
+//   0  Knuth's branch-free TwoSum, 6 DADD;
+//   1  operands ordered by magnitude (one DSETP with |.| modifiers, two 64-bit selects), then
+//      Dekker's Fast2Sum, exact for |x| >= |y| — 3 DADD + 1 DSETP;
+//   2  ordered by the sign-masked high words (exponent first: Fast2Sum is exact whenever
+//      e_x >= e_y in radix 2), integer compare — 3 DADD, no extra FP64 instruction.
+#ifndef PJB_TWOSUM
+#define PJB_TWOSUM 0
+#endif
 __device__ __forceinline__ DD two_sum(double a, double b) {
+#if PJB_TWOSUM == 0
     double s = __dadd_rn(a, b);
     double bb = __dsub_rn(s, a);
     double e = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
     return {s, e};
+#else
+#if PJB_TWOSUM == 1
+    const bool c = fabs(a) >= fabs(b);
+#else
+    const bool c = (__double2hiint(a) & 0x7fffffff) >= (__double2hiint(b) & 0x7fffffff);
+#endif
+    const double x = c ? a : b, y = c ? b : a;
+    const double s = __dadd_rn(x, y);
+    return {s, __dsub_rn(y, __dsub_rn(s, x))};
+#endif
 }
 __device__ __forceinline__ DD fast_two_sum(double a, double b) {
     double s = __dadd_rn(a, b);

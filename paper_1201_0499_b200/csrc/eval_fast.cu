@@ -71,6 +71,9 @@ __device__ __forceinline__ bool fin(const CDD& v) {
 
 // NS: compile-time plane stride of the shared-memory point tables (>= n), so that the four
 // component loads of a gather share one address register (immediate offsets).
+#ifndef PJB_D2_SUFFIX
+#define PJB_D2_SUFFIX 1
+#endif
 // Register budget: 3 CTAs x 256 threads (<= 85 registers) for k <= 12, where the per-warp
 // staging also fits three CTAs; 2 CTAs (<= 128 registers) above. Measured with tools/tune.py:
 // k = 8: 0.853 (3 CTAs) vs 0.843 (2 CTAs); k = 16: 0.763 (2 CTAs) vs 0.723 (3 CTAs).
@@ -112,6 +115,9 @@ __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) f
             st_hl(tab + t * tabPt + 2 * v, 2 * NS, x);
         }
         __syncthreads();
+#ifdef PJB_STAGGER
+        if (warp & 1) __nanosleep(PJB_STAGGER);  // experiment: desynchronise the CTA's warps
+#endif
         if (!D2) {  // power chains, ref kernels.cpp:16-24 (normalised products: shared table)
             for (int i = threadIdx.x; i < tp * n; i += blockDim.x) {
                 const int t = i / n, v = i - t * n;
@@ -187,6 +193,51 @@ __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) f
                 };
                 auto SLOT = [&](int j) -> double* { return stg + j * W * 32 + 2 * lane; };
 
+#if PJB_D2_SUFFIX
+                if constexpr (D2) {
+                // ---- stage 1 (d <= 2): suffix products B_j = v_{j+1}...v_{k-1}, staged in slot j.
+                // The host orders each monomial's variables with the a_j = 2 ones last
+                // (order_variables), so the common factor f = prod over a_j = 2 of x_j is the suffix
+                // product B_{k-1-c_g} (c_g = the number of a_j = 2): no separate factor chain —
+                // 3k-2 complex products per monomial instead of 4k-3 (22 vs 29 at k = 8).
+                // Chain states are compile-time: B_j is normalised iff k-2-j is even.
+                int cg = 0;
+#pragma unroll
+                for (int j = 0; j < K; ++j) cg += EX1(j) & 1;
+                // (registers are tight at 3 CTAs/SM: x values and B_0 are re-gathered from shared
+                // memory at their second use rather than kept live)
+                st_hl(SLOT(K - 1), 64, one);  // B_{k-1} = 1: f for c_g = 0
+                CDD B0 = X(K - 1);
+                st_hl(SLOT(K - 2), 64, B0);
+#pragma unroll
+                for (int j = K - 3; j >= 0; --j) {
+                    B0 = cmul_n(((K - 3 - j) & 1) != 0, B0, X(j + 1));
+                    st_hl(SLOT(j), 64, B0);
+                }
+                CDD f = ld_hl(SLOT(max(K - 1 - cg, 0)), 64);
+                if (__any_sync(0xffffffffu, cg == K)) {  // every exponent 2: f = B_0 * v_0
+                    const CDD fa = cdd_mul(B0, X(0));
+                    if (cg == K) f = fa;
+                }
+                // ---- stage 2 (d <= 2): prefix chain seeded with the coefficient and the factor,
+                // F'_0 = f*c, F'_{j+1} = F'_j * v_j; every derivative L'_j = F'_j * B_j (slot j)
+                // carries c and f; power rule a_j * L'_j exact; value F'_{k-1} * v_{k-1}
+                // (ref kernels.cpp:108-118 order: value after the factor). F'_j normalised iff j even.
+                const CDD cval = {__ldg(cf), __ldg(cf + 32), __ldg(cf + 64), __ldg(cf + 96)};
+                CDD Fp = cdd_mul(f, cval);
+                st_hl(SLOT(0), 64, SCALE(0, cdd_mul_u(Fp, B0)));
+#pragma unroll
+                for (int j = 1; j < K; ++j) {
+                    Fp = cmul_n(((j - 1) & 1) != 0, Fp, X(j - 1));
+                    if (j < K - 1) {
+                        const CDD L = cdd_mul_u(Fp, ld_hl(SLOT(j), 64));
+                        st_hl(SLOT(j), 64, SCALE(j, L));
+                    }
+                }
+                st_hl(SLOT(K - 1), 64, SCALE(K - 1, Fp));
+                st_hl(SLOT(K), 64, cdd_mul(Fp, X(K - 1)));
+                } else {
+#endif
                 // ---- stage 1 + forward products (interleaved chains); chain states are
                 // compile-time after unrolling: F_j is normalised iff j is odd, f_j iff j is even;
                 // a product renormalises iff its chain input is not normalised
@@ -230,6 +281,9 @@ __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) f
                     q = cmul_n(!q_norm, q, X(j));
                 }
                 st_hl(SLOT(0), 64, SCALE(0, q));
+#if PJB_D2_SUFFIX
+                }
+#endif
                 __syncwarp();
                 // ---- stage 3, phase 1: balanced segmented sums. The (row, chunk) schedule
                 // hands every lane R consecutive entries of the output-major, ascending-g list

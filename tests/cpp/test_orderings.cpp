@@ -63,13 +63,23 @@ static void test_system(int n, int m, int k, int d, uint64_t seed) {
             const int gl = std::min(32, m - ch * 32);
             std::vector<int32_t> pos(P.begin() + (size_t(p) * m + ch * 32) * k,
                                      P.begin() + (size_t(p) * m + ch * 32 + gl) * k);
+            std::vector<int32_t> ex(E.begin() + (size_t(p) * m + ch * 32) * k,
+                                    E.begin() + (size_t(p) * m + ch * 32 + gl) * k);
             std::vector<uint8_t> perm, ident(size_t(gl) * k);
-            order_variables(pos.data(), gl, k, p * C + ch, perm);
+            // d <= 2: exponent-2 variables last (the kernel's suffix-product factor), swaps in-group
+            order_variables(pos.data(), d <= 2 ? ex.data() : nullptr, gl, k, p * C + ch, perm);
             for (int g = 0; g < gl; ++g) {
                 std::set<int> s;
+                int at = 0;
+                for (int pass = 0; pass < (d <= 2 ? 2 : 1); ++pass)
+                    for (int j = 0; j < k; ++j)
+                        if (d > 2 || (ex[size_t(g) * k + j] == 1) == (pass == 0)) ident[g * k + at++] = uint8_t(j);
+                bool seen2 = false;
                 for (int j = 0; j < k; ++j) {
                     s.insert(perm[g * k + j]);
-                    ident[g * k + j] = uint8_t(j);
+                    const bool two = ex[size_t(g) * k + perm[g * k + j]] == 2;
+                    if (d <= 2) CHECK(!seen2 || two);  // once an exponent-2 variable, only those
+                    seen2 = seen2 || two;
                 }
                 CHECK(int(s.size()) == k && *s.rbegin() == k - 1);
             }
