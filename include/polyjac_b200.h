@@ -241,12 +241,13 @@ int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double*
 int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points);
 /* Advanced: kernel choice for complex double (PJ_PREC_D) or the fast dd order. 0 = automatic,
  * -1 = the generic kernel (eval_kernels.cu), 1 = the k-specialised kernel (eval_fastd.cu for complex
- * double, eval_fast.cu for dd). Every choice satisfies the same contract (complex double:
- * bit-exact with the reference). With PJ_OP_NEWTON: the Newton solve, -1 = the column kernel,
+ * double, eval_fast.cu for dd), 3 = the warp-specialised dd kernel (eval_fast_ws.cu: producer and
+ * consumer warps; d <= 2, m <= 32, n <= 64, k <= 12; bit-identical with variant 1). Every choice
+ * satisfies the same contract (complex double: bit-exact with the reference). With PJ_OP_NEWTON: the Newton solve, -1 = the column kernel,
  * 1 = the panel kernel (n <= 32); both give identical bits. */
 int pj_set_kernel_variant(pj_ctx* ctx, int flags, int variant);
 /* Report the launch shape used for `flags`: threads, tile points, blocks, dynamic smem bytes,
- * kernel (-1 = generic, 1 = fast dd, 2 = fast complex double; with PJ_OP_NEWTON: 0 = column kernel,
+ * kernel (-1 = generic, 1 = fast dd, 2 = fast complex double, 3 = warp-specialised dd; with PJ_OP_NEWTON: 0 = column kernel,
  * 1 = panel kernel, 2 = column kernel on global slabs). */
 int pj_get_launch(pj_ctx* ctx, int flags, int32_t* threads, int32_t* tile_points, int32_t* blocks,
                   int64_t* smem_bytes, int32_t* variant);

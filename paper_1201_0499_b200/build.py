@@ -19,9 +19,9 @@ CLI = os.path.join(HERE, "polyjac_b200")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
-CU = ["eval_kernels.cu", "eval_fast.cu", "eval_fastd.cu", "newton.cu", "fp64_probe.cu"]
+CU = ["eval_kernels.cu", "eval_fast.cu", "eval_fast_ws.cu", "eval_fastd.cu", "newton.cu", "fp64_probe.cu"]
 CPP = ["capi.cpp", "sysio.cpp"]
-HEADERS = ["dd.cuh", "eval_kernels.h"]
+HEADERS = ["dd.cuh", "eval_kernels.h", "fast_common.cuh"]
 
 
 def _newer(target, deps):
@@ -49,8 +49,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
                "-fmad=false", "-Xptxas", "-v", "-c", src, "-o", obj]
         ks = os.environ.get("PJB_FAST_KS")  # developer shortcut: e.g. "8,16" (default: 2..16)
-        if ks and f == "eval_fast.cu":
-            cmd.insert(-4, "-DPJB_FAST_KS(X)=" + " ".join(f"X({k})" for k in ks.split(",")))
+        if ks and f in ("eval_fast.cu", "eval_fast_ws.cu"):
+            mac = "PJB_FAST_KS" if f == "eval_fast.cu" else "PJB_WS_KS"
+            cmd.insert(-4, f"-D{mac}(X)=" + " ".join(f"X({k})" for k in ks.split(",") if f == "eval_fast.cu" or int(k) <= 12))
         stamp = obj + ".cmd"
         old = open(stamp).read() if os.path.exists(stamp) else ""
         if force or old != " ".join(cmd) or _newer(obj, [src] + hdrs):

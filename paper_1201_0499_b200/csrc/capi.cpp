@@ -10,6 +10,7 @@
 #include <exception>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <random>
 #include <string>
@@ -588,7 +589,26 @@ int choose_launch(pj_ctx* c, int mode) {
             best.gscratch = nullptr;
         }
     };
-    if (mode == kModeDDFast && !c->wide && !c->ragged && pjb::fast_supported(c->k) && M.over_variant >= 0) {
+    if (mode == kModeDDFast && !c->wide && !c->ragged && pjb::fast_ws_supported(c->k, c->n, c->m, c->d) &&
+        M.over_variant == 3) {
+        // warp-specialised kernel (eval_fast_ws.cu, opt-in): 8-warp CTAs split into producers and
+        // consumers, 2-point tiles (the ring of 8 staging buffers and its counters fill shared
+        // memory). Measured at C2: 4 : 4 best, 10.49 M evals/s against 11.10 M
+        // for the fused kernel, so the automatic choice stays with the fused kernel.
+        const char* ev = std::getenv("PJ_WS_PRODUCERS");  // developer knob (A/B of the split)
+        const int np = ev ? std::atoi(ev) : 4;
+        std::vector<int> ftps = M.over_tp ? tps : std::vector<int>{2, 1};
+        const int nw = M.over_threads ? M.over_threads / 32 : 8;
+        for (size_t i = 0; i < ftps.size() && np > 0 && np < nw && nw <= 8; ++i) {
+            const size_t sm = pjb::fast_ws_smem(c->n, c->k, nw, ftps[i]);
+            if (sm > c->smem_optin) continue;
+            const int before = best_score;
+            consider(3, nw, ftps[i], sm, pjb::fast_ws_blocks_per_sm(c->k, c->n, nw * 32, sm), 100 + int(ftps.size() - i));
+            if (best_score != before) best.producers = np;
+        }
+    }
+    if (mode == kModeDDFast && !c->wide && !c->ragged && pjb::fast_supported(c->k) && M.over_variant >= 0 &&
+        best_score < 0) {
         // measured (tools/tune.py, tools/tp_test.py): 8-warp CTAs beat more, smaller CTAs at
         // equal residency. Tiles: with 3 CTAs per SM (k <= 12) a 3-point tile uses the last
         // shared-memory slack and cuts the tile barriers per point (C2: 9.30 vs 9.27 M evals/s for
@@ -1395,6 +1415,8 @@ int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, d
     }
     cudaError_t e = L.variant == 1 ? pjb::launch_fast(ctx->k, L, ctx->dev_fast(), d_points, d_out, (long long)batch,
                                                      (cudaStream_t)stream)
+                    : L.variant == 3 ? pjb::launch_fast_ws(ctx->k, L, ctx->dev_fast(), d_points, d_out, (long long)batch,
+                                                           (cudaStream_t)stream)
                     : L.variant == 2 ? pjb::launch_fastd(ctx->k, L, ctx->dev_fastd(), d_points, d_out, (long long)batch,
                                                          (cudaStream_t)stream)
                                      : pjb::launch_eval(pi + 1, order_of(flags), L, ctx->dev(pi), d_points, d_out,
@@ -1824,7 +1846,10 @@ int pj_set_kernel_variant(pj_ctx* ctx, int flags, int variant) {
     }
     const int md = mode_of(flags);
     if (md == kModeDDRef) return fail(PJ_EINVAL, "kernel variants exist for complex double and the fast dd order");
-    if (variant > 1 || variant < -1) return fail(PJ_EINVAL, "unknown kernel variant");
+    if ((variant > 1 && !(variant == 3 && md == kModeDDFast)) || variant < -1)
+        return fail(PJ_EINVAL, "unknown kernel variant");
+    if (variant == 3 && !pjb::fast_ws_supported(ctx->k, ctx->n, ctx->m, ctx->d))
+        return fail(PJ_EINVAL, "the warp-specialised kernel needs d <= 2, m <= 32, n <= 64, k in [2, 12]");
     if (variant == 1 && md == kModeDDFast && !pjb::fast_supported(ctx->k))
         return fail(PJ_EINVAL, "no specialised kernel for this k");
     if (variant == 1 && md == kModeD && !pjb::fastd_supported(ctx->k))

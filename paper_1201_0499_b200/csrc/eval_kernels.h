@@ -70,6 +70,7 @@ struct LaunchCfg {
     size_t smem_bytes = 0;    // dynamic shared memory (0 in global-scratch mode)
     double* gscratch = nullptr;  // non-null: tables/staging in global memory (huge systems)
     int* flag = nullptr;      // device int, set to 1 on a non-finite coordinate
+    int producers = 0;        // warp-specialised dd kernel (variant 3): producer warps per CTA
 };
 
 cudaError_t launch_eval(int prec, int order, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out,
@@ -91,6 +92,13 @@ int fast_plane_stride(int n);
 cudaError_t launch_fast(int k, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
                         cudaStream_t st);
 int fast_blocks_per_sm(int k, int n, int d, int threads, size_t smem);
+
+// warp-specialised fast complex-dd kernel (eval_fast_ws.cu): d <= 2, m <= 32, n <= 64, k in [2, 12]
+bool fast_ws_supported(int k, int n, int m, int d);
+size_t fast_ws_smem(int n, int k, int nw, int tp);
+cudaError_t launch_fast_ws(int k, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
+                           cudaStream_t st);
+int fast_ws_blocks_per_sm(int k, int n, int threads, size_t smem);
 
 // fast complex-double kernels in the reference order (eval_fastd.cu), k in [1, 16], byte encoding
 bool fastd_supported(int k);

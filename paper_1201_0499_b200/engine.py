@@ -717,7 +717,8 @@ class EvaluationContext:
 
     def set_variant(self, variant: int, precision: str = "dd", newton: bool = False) -> None:
         """Kernel choice (pj_set_kernel_variant) for complex double ("d") or the fast dd order:
-        0 auto, -1 generic, 1 k-specialised; newton=True: the Newton solve (-1 column kernel,
+        0 auto, -1 generic, 1 k-specialised, 3 warp-specialised (dd, d <= 2, m <= 32, n <= 64,
+        k <= 12); newton=True: the Newton solve (-1 column kernel,
         1 panel kernel for n <= 32)."""
         f = _flags(precision, None) | (_lib.PJ_OP_NEWTON if newton else 0)
         check(lib().pj_set_kernel_variant(self._h, f, variant))

@@ -8,7 +8,7 @@ B=paper_1201_0499_b200/_build
 F=$1; shift
 mkdir -p tools/_exp
 objs=""
-for o in eval_kernels.cu eval_fast.cu eval_fastd.cu newton.cu fp64_probe.cu capi.cpp sysio.cpp; do
+for o in eval_kernels.cu eval_fast.cu eval_fast_ws.cu eval_fastd.cu newton.cu fp64_probe.cu capi.cpp sysio.cpp; do
   [ "$o" = "$F" ] || objs="$objs $B/$o.o"
 done
 for spec in "$@"; do
