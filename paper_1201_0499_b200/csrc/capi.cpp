@@ -703,7 +703,7 @@ int newton_plan(pj_ctx* c, int pi, pj_ctx::NewtonPlan** out) {
         P.panel = pjb::newton_panel_supported(c->n) && P.over_variant == 1 && mb + ib <= c->smem_optin;
         if (P.panel) P.threads = std::max(P.threads, 64);  // one look-ahead warp + updaters
         if (mb + ib <= c->smem_optin) {
-            const int nb = pjb::newton_blocks_per_sm(prec, c->n, P.threads, mb + ib, P.panel);
+            const int nb = pjb::newton_blocks_per_sm(prec, c->n, P.threads, mb + ib, P.panel, false);
             if (nb > 0) {
                 P.smem = mb + ib;
                 P.blocks = nb * c->sms;
@@ -712,7 +712,7 @@ int newton_plan(pj_ctx* c, int pi, pj_ctx::NewtonPlan** out) {
         }
         if (!P.blocks) {  // augmented matrix beyond shared memory: per-CTA slabs in HBM (L2-resident)
             P.panel = false;
-            const int nb = std::max(1, std::min(pjb::newton_blocks_per_sm(prec, c->n, P.threads, ib, false), 4));
+            const int nb = std::max(1, std::min(pjb::newton_blocks_per_sm(prec, c->n, P.threads, ib, false, true), 4));
             P.smem = ib;
             P.blocks = nb * c->sms;
             P.gscr = true;

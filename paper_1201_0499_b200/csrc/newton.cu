@@ -142,22 +142,44 @@ __device__ __forceinline__ CDD shfl_idx<CDD>(CDD v, int src) {
 }
 
 // ---- pieces shared by the two Newton kernels
-// Load [J | y − f] of point b (all threads; warp 0 the right-hand side, its norm, the identity row
-// list). Shared-memory matrices: 8-byte cp.async copies straight into the pair layout (no
+// Load [J | y − f] of point b (all threads; role warp 0 the right-hand side, its norm, the identity
+// row list). Shared-memory matrices: 8-byte cp.async copies straight into the pair layout (no
 // registers, every copy in flight at once); global slabs: plain loads. The caller waits + syncs.
-template <class T>
-__device__ __forceinline__ void nt_load(const NewtonArgs& a, long long b, double* A, int* list, int* sing) {
+template <class T, bool GS = false>
+__device__ __forceinline__ void nt_load(const NewtonArgs& a, long long b, double* A, int* list, int* sing,
+                                        int warp) {
     using S = Sc<T>;
     constexpr int W = S::W;
     const int n = a.n, ld = n + 1, P = n * ld;
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
     const double* ev = a.evals + size_t(b) * (size_t(n) * n + n) * W;
-    if (!a.gscratch) {
-        for (int t = tid; t < n * n * W; t += nt) {
-            const int el = t / W, comp = t - el * W;
-            const int i = el / n, j = el - i * n;
+    if (!GS) {
+        // word t = (element el = i * n + j, component t mod W); the thread's (i, j) advance by a fixed
+        // stride (nt / W elements), so the loop carries no integer division (it used to dominate
+        // the load phase: ~1.2k instructions per thread and point)
+        const int es = nt / W, di = es / n, dj = es - di * n;
+        int el = tid / W;
+        const int comp = tid - el * W;
+        int i = el / n, j = el - i * n;
+        const double* src = ev + size_t(n) * W + tid;
+#if PJB_NT_LDX == 1  // timing experiment: no matrix load at all (results wrong)
+        if (0)
+#elif PJB_NT_LDX == 2  // timing experiment: 16-byte copies into a wrong layout (results wrong)
+        for (int t = 2 * tid; t < n * n * W; t += 2 * nt) {
+            const unsigned dst = unsigned(__cvta_generic_to_shared(A + t));
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(dst), "l"(ev + size_t(n) * W + t));
+        }
+        if (0)
+#endif
+        for (int t = tid; t < n * n * W; t += nt, src += nt) {
             const unsigned dst = unsigned(__cvta_generic_to_shared(A + NL<T>::off(i * ld + j, comp, P)));
-            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(ev + size_t(n) * W + t));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(src));
+            i += di;
+            j += dj;
+            if (j >= n) {
+                j -= n;
+                ++i;
+            }
         }
         asm volatile("cp.async.commit_group;\n" ::);
     } else {
@@ -247,6 +269,12 @@ __device__ __forceinline__ void nt_back_substitute(const NewtonArgs& a, long lon
 // kRecip[c] = ceil(2^16 / c): floor(x / c) == (x * kRecip[c]) >> 16 for x, c <= 256
 __constant__ unsigned kRecip[257];
 
+#ifndef PJB_NT_ROTATE
+#define PJB_NT_ROTATE 1
+#endif
+#ifndef PJB_NT_PREFETCH
+#define PJB_NT_PREFETCH 1
+#endif
 #ifndef PJB_NT_MINB
 #define PJB_NT_MINB 6
 #endif
@@ -263,21 +291,38 @@ struct NtBounds {
 // 2.45 (7) and 2.60 (6) at C2)
 template <class T, int NQ>
 constexpr int nt_min_blocks() { return NQ == 1 && Sc<T>::W == 2 ? PJB_NT_MINB_D : NtBounds<NQ>::blocks; }
-template <class T, int NQ>
+// GS: the matrix lives in a per-CTA global slab (a.gscratch) instead of shared memory. A separate
+// instantiation, so that in the shared-memory kernel the compiler sees every matrix access as a
+// shared-memory access (LDS/STS, not generic LD/ST that must resolve the address space at run time)
+template <class T, int NQ, bool GS>
 __global__ void __launch_bounds__(NtBounds<NQ>::threads, nt_min_blocks<T, NQ>()) newton_kernel(NewtonArgs a) {
     using S = Sc<T>;
     constexpr int W = S::W;
     extern __shared__ __align__(16) double smem[];
-    __shared__ int s_sing;
+    __shared__ int s_sing, s_la;
     const int n = a.n, ld = n + 1, P = n * ld;
-    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    // Warp roles. A warp's SM sub-partition (scheduler) is its hardware warp slot mod 4, and a CTA's
+    // warps occupy consecutive slots: with a fixed look-ahead warp every co-resident CTA would put
+    // its latency-critical look-ahead chain (and the back substitution) on the same scheduler. The
+    // role-0 warp is therefore the CTA's warp (slot group of warp 0) mod nw, which spreads the
+    // chains of the CTAs sharing an SM over the schedulers.
+    if (tid == 0) {
+        unsigned wid = 0;
+#if PJB_NT_ROTATE
+        asm volatile("mov.u32 %0, %%warpid;" : "=r"(wid));
+#endif
+        s_la = int((wid >> 2) % unsigned(blockDim.x >> 5));
+    }
+    __syncthreads();
+    const int nw = nt >> 5, warp = ((tid >> 5) - s_la + nw) % nw;  // role index: 0 = look-ahead
     // dynamic shared memory: ints (pivot rows, pivot step of each row, two active-row lists), then
     // the matrix planes unless they live in a global slab
     int* s_piv = reinterpret_cast<int*>(smem);
     int* s_step = s_piv + n;
     int* s_list0 = s_step + n;
     int* s_list1 = s_list0 + n;
-    double* A = a.gscratch ? a.gscratch + size_t(blockIdx.x) * a.gstride : smem + newton_int_words(n);
+    double* A = GS ? a.gscratch + size_t(blockIdx.x) * a.gstride : smem + newton_int_words(n);
     double* INV = A + size_t(W) * P;  // [W][n] pivot inverses
     double* DX = INV + size_t(W) * n;   // [W][n] solution
 
@@ -350,10 +395,34 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, nt_min_blocks<T, NQ>())
         }
         PJB_TSUB(c, 3)
     };
+#ifdef PJB_NT_PHASES
+    // developer instrumentation: per-CTA cycle totals of the load, elimination and back-substitution
+    // phases over all of its points, after the B status words (status must hold B + 2 + 8 * grid)
+    long long ph[4] = {0, 0, 0, 0};
+    long long tph = clock64();
+#define PJB_PH(i)                      \
+    {                                  \
+        const long long t_ = clock64(); \
+        ph[i] += t_ - tph;             \
+        tph = t_;                      \
+    }
+#else
+#define PJB_PH(i)
+#endif
     for (long long b = blockIdx.x; b < a.B; b += gridDim.x) {
-        nt_load<T>(a, b, A, s_list0, &s_sing);
+        nt_load<T, GS>(a, b, A, s_list0, &s_sing, warp);
         asm volatile("cp.async.wait_all;\n" ::);
         __syncthreads();
+        PJB_PH(0)
+#if PJB_NT_PREFETCH
+        // pull the CTA's next point into L2 while this one is eliminated: its load then waits on L2
+        // instead of DRAM (measured: the load phase took ~25k cycles per point under full load)
+        if (b + gridDim.x < a.B) {
+            const char* nx = reinterpret_cast<const char*>(a.evals + size_t(b + gridDim.x) * (size_t(n) * n + n) * W);
+            const int lines = int((size_t(n) * n + n) * W * sizeof(double) / 128);
+            for (int l = tid; l < lines; l += nt) asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + size_t(l) * 128));
+        }
+#endif
         // ---- column 0: pivot, inverse, multipliers
         if (warp == 0) {
             T v[NQ];
@@ -409,7 +478,7 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, nt_min_blocks<T, NQ>())
             } else {
                 // columns kk+2..n (Cp of them) for R rows: a thread keeps u = A[pr][j] in registers
                 // and walks rows rg, rg+G, ...
-                const int Cp = n - kk - 1, Tp = nt - 32, tp = tid - 32;
+                const int Cp = n - kk - 1, Tp = nt - 32, tp = (warp - 1) * 32 + lane;
                 // measured (tools/nt_quick.py, C2/C3): column pairs win for complex double and
                 // n > 32 (n = 64 dd: 8.92 -> 8.40 ms), single columns for n <= 32 dd (7.80 vs 8.42 ms)
                 constexpr bool kPairs = NQ >= 2 || W == 2;
@@ -461,9 +530,21 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, nt_min_blocks<T, NQ>())
             singular = s_sing != 0;
         }
 
+        PJB_PH(1)
         if (warp == 0) nt_back_substitute<T, NQ>(a, b, A, INV, DX, s_piv, s_step, singular);
         __syncthreads();  // the next point reuses the matrix storage
+        PJB_PH(2)
+#ifdef PJB_NT_PHASES
+        ++ph[3];
+#endif
     }
+#ifdef PJB_NT_PHASES
+    if (tid == 0 && a.status) {
+        long long* o = reinterpret_cast<long long*>(a.status + ((a.B + 1) & ~1LL)) + 4 * blockIdx.x;
+        for (int i = 0; i < 4; ++i) o[i] = ph[i];
+    }
+#endif
+#undef PJB_PH
 }
 
 // ---- blocked variant for n <= 32 (opt-in, pj_set_kernel_variant with PJ_OP_NEWTON): the
@@ -499,7 +580,7 @@ __global__ void __launch_bounds__(128, PJB_NTP_MINB) newton_panel_kernel(NewtonA
     const bool valid = lane < n;  // warp 0: lane = row
 
     for (long long b = blockIdx.x; b < a.B; b += gridDim.x) {
-        nt_load<T>(a, b, A, s_list[0], &s_sing);
+        nt_load<T>(a, b, A, s_list[0], &s_sing, warp);
         if (warp == 0)
             for (int i = lane; i < n; i += 32) s_step[i] = n;  // n = not yet pivoted
         asm volatile("cp.async.wait_all;\n" ::);
@@ -657,18 +738,20 @@ __global__ void __launch_bounds__(128, PJB_NTP_MINB) newton_panel_kernel(NewtonA
 }
 
 template <class T>
-const void* newton_fn(int nq) {
+const void* newton_fn(int nq, bool gs) {
+    if (gs) return nq <= 4 ? (const void*)newton_kernel<T, 4, true> : (const void*)newton_kernel<T, 8, true>;
     switch (nq) {
-        case 1: return (const void*)newton_kernel<T, 1>;
-        case 2: return (const void*)newton_kernel<T, 2>;
-        case 4: return (const void*)newton_kernel<T, 4>;
-        default: return (const void*)newton_kernel<T, 8>;
+        case 1: return (const void*)newton_kernel<T, 1, false>;
+        case 2: return (const void*)newton_kernel<T, 2, false>;
+        case 4: return (const void*)newton_kernel<T, 4, false>;
+        default: return (const void*)newton_kernel<T, 8, false>;
     }
 }
+// (a global-slab launch with n <= 64 runs the NQ = 4 instantiation: same code, more row slots)
 int nq_of(int n) { return n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : 8; }
-const void* fn_of(int prec, int n, bool panel) {
-    if (panel) return prec == 1 ? (const void*)newton_panel_kernel<CD> : (const void*)newton_panel_kernel<CDD>;
-    return prec == 1 ? newton_fn<CD>(nq_of(n)) : newton_fn<CDD>(nq_of(n));
+const void* fn_of(int prec, int n, bool panel, bool gs) {
+    if (panel && !gs) return prec == 1 ? (const void*)newton_panel_kernel<CD> : (const void*)newton_panel_kernel<CDD>;
+    return prec == 1 ? newton_fn<CD>(nq_of(n), gs) : newton_fn<CDD>(nq_of(n), gs);
 }
 
 }  // namespace
@@ -698,8 +781,8 @@ static cudaError_t init_recip() {
 
 bool newton_panel_supported(int n) { return n <= 32; }
 
-int newton_blocks_per_sm(int prec, int n, int threads, size_t smem, bool panel) {
-    const void* f = fn_of(prec, n, panel);
+int newton_blocks_per_sm(int prec, int n, int threads, size_t smem, bool panel, bool gs) {
+    const void* f = fn_of(prec, n, panel, gs);
     if (smem) cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_limit(f));
     int nb = 0;
     if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, threads, smem) != cudaSuccess) return 0;
@@ -709,7 +792,7 @@ int newton_blocks_per_sm(int prec, int n, int threads, size_t smem, bool panel) 
 cudaError_t launch_newton(int prec, const NewtonArgs& args, int blocks, int threads, size_t smem, bool panel,
                           cudaStream_t st) {
     if (args.B <= 0) return cudaSuccess;
-    const void* f = fn_of(prec, args.n, panel && !args.gscratch);
+    const void* f = fn_of(prec, args.n, panel, args.gscratch != nullptr);
     if (cudaError_t e = init_recip()) return e;
     if (smem) {
         cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_limit(f));
