@@ -697,8 +697,8 @@ int newton_plan(pj_ctx* c, int pi, pj_ctx::NewtonPlan** out) {
     const size_t mb = pjb::newton_matrix_bytes(prec, c->n), ib = pjb::newton_int_bytes(c->n);
     if (!P.blocks) {
         // n <= 32: 128-thread CTAs (the kernel is compiled for at most 128 there, newton.cu)
-        P.threads = P.over_threads ? P.over_threads : (c->n <= 32 ? 128 : 256);
-        if (c->n <= 32) P.threads = std::min(P.threads, 128);
+        P.threads = P.over_threads ? P.over_threads : pjb::newton_max_threads(c->n);
+        P.threads = std::min(P.threads, pjb::newton_max_threads(c->n));
         // the panel kernel is opt-in: measured slower at C2 (dd 10.7 vs 7.2 ms, d 2.50 vs 2.44 ms)
         P.panel = pjb::newton_panel_supported(c->n) && P.over_variant == 1 && mb + ib <= c->smem_optin;
         if (P.panel) P.threads = std::max(P.threads, 64);  // one look-ahead warp + updaters

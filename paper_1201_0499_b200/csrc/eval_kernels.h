@@ -125,6 +125,7 @@ size_t newton_matrix_bytes(int prec, int n);  // matrix planes, inverses, soluti
 size_t newton_int_bytes(int n);               // pivot bookkeeping (always in shared memory)
 // panel = the blocked kernel for n <= 32 (newton_panel_kernel), else the column kernel
 bool newton_panel_supported(int n);
+int newton_max_threads(int n);  // the column kernel's launch bound for this n
 // gs: the matrix in per-CTA global slabs (a separate kernel instantiation)
 int newton_blocks_per_sm(int prec, int n, int threads, size_t smem, bool panel, bool gs);
 cudaError_t launch_newton(int prec, const NewtonArgs& args, int blocks, int threads, size_t smem, bool panel,

@@ -278,11 +278,14 @@ __constant__ unsigned kRecip[257];
 #ifndef PJB_NT_MINB
 #define PJB_NT_MINB 6
 #endif
+#ifndef PJB_NT_T1
+#define PJB_NT_T1 128
+#endif
 // n <= 32 (NQ = 1) runs 128-thread CTAs, six per SM (the matrix is 36 KB in dd): 85 registers
 template <int NQ>
 struct NtBounds {
     // (measured: 160-thread CTAs, four per SM: n = 32 dd -2.7%, complex double +22% time)
-    static constexpr int threads = NQ == 1 ? 128 : 256, blocks = NQ == 1 ? PJB_NT_MINB : 1;
+    static constexpr int threads = NQ == 1 ? PJB_NT_T1 : 256, blocks = NQ == 1 ? PJB_NT_MINB : 1;
 };
 #ifndef PJB_NT_MINB_D
 #define PJB_NT_MINB_D 8
@@ -780,6 +783,7 @@ static cudaError_t init_recip() {
 }
 
 bool newton_panel_supported(int n) { return n <= 32; }
+int newton_max_threads(int n) { return n <= 32 ? NtBounds<1>::threads : NtBounds<2>::threads; }
 
 int newton_blocks_per_sm(int prec, int n, int threads, size_t smem, bool panel, bool gs) {
     const void* f = fn_of(prec, n, panel, gs);
