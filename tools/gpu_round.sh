@@ -11,4 +11,8 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 3 --warmup 3 --e2e-steps 1 --no-cpu-baseline > gpurun_out/${TAG}_ncu_bench.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fast_kernel|eval_kernel" -s 3 -c 1 \
     -o gpurun_out/${TAG}_prof python bench.py --steps 1 --warmup 3 --e2e-steps 1 --no-cpu-baseline > gpurun_out/${TAG}_ncu_full.log 2>&1
-echo done
+echo done eval
+# Newton solve (f1) capture of the same build
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:newton_kernel -s 1 -c 1 \
+    -o gpurun_out/${TAG}_newton_prof python tools/newton_prof.py > gpurun_out/${TAG}_newton_ncu.log 2>&1
+echo done newton
