@@ -42,8 +42,16 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* a) {
 __device__ __forceinline__ void st_release(unsigned* a, unsigned v) {
     asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(a)), "r"(v) : "memory");
 }
+#ifndef PJB_WS_BACKOFF
+#define PJB_WS_BACKOFF 256
+#endif
+// a waiting warp backs off between polls (nanosleep) so its spin does not take issue slots from
+// the producers on the same scheduler
 __device__ __forceinline__ void wait_at_least(const unsigned* a, unsigned v) {
     while (ld_acquire(a) < v) {
+#if PJB_WS_BACKOFF
+        __nanosleep(PJB_WS_BACKOFF);
+#endif
     }
 }
 // every lane's shared-memory accesses to the buffer are ordered before lane 0's release
