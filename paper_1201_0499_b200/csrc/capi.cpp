@@ -440,6 +440,11 @@ struct pj_ctx {
     double* d_in[kHostStreams] = {};
     double* d_out[kHostStreams] = {};
     size_t in_cap = 0, out_cap = 0;
+    // small host batches (pj_evaluate_host, <= kSmallOut result bytes): page-locked staging
+    // [points | results | flag], so the call is two async copies, the kernel and one sync
+    static constexpr size_t kSmallOut = size_t(1) << 20;
+    char* h_small = nullptr;
+    size_t h_small_in = 0;  // bytes of the points part (results follow, then one int)
     cudaStream_t hstream[kHostStreams] = {};
     cudaEvent_t hdone[kHostStreams] = {};
     cudaEvent_t nfork = nullptr;  // pj_newton_step fork event
@@ -543,6 +548,7 @@ void free_ctx(pj_ctx* c) {
         if (c->hdone[i]) cudaEventDestroy(c->hdone[i]);
     }
     if (c->nfork) cudaEventDestroy(c->nfork);
+    if (c->h_small) cudaFreeHost(c->h_small);
     cudaSetDevice(prev);
     delete c;
 }
@@ -1413,6 +1419,21 @@ int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, d
             return fail(PJ_ENONFINITE, "evaluate: non-finite coordinate");
         }
     }
+    if (L.variant == 1) {
+        // a batch with fewer tiles than CTAs (C1: one point) spreads each tile's tasks over
+        // several CTAs, one task per warp at most, instead of leaving all but a few SMs idle; the
+        // grid shrinks to the CTAs that have work (a multiple of the split, eval_fast.cu). (The
+        // complex-double kernel keeps one CTA per tile: its 128-register budget has no room for
+        // the split's loop state.)
+        const long long ntiles = (batch + L.tp - 1) / L.tp;
+        if (ntiles < L.blocks) {
+            const long long in_tile = std::min<long long>(batch, L.tp);
+            const long long tasks = in_tile * ctx->n;
+            const long long nw = L.threads / 32;
+            L.splits = int(std::max(1LL, std::min<long long>(L.blocks / ntiles, (tasks + nw - 1) / nw)));
+            L.blocks = int(std::min<long long>(L.blocks, ntiles * L.splits));
+        }
+    }
     cudaError_t e = L.variant == 1 ? pjb::launch_fast(ctx->k, L, ctx->dev_fast(), d_points, d_out, (long long)batch,
                                                      (cudaStream_t)stream)
                     : L.variant == 3 ? pjb::launch_fast_ws(ctx->k, L, ctx->dev_fast(), d_points, d_out, (long long)batch,
@@ -1475,9 +1496,13 @@ int pj_evaluate_host(pj_ctx* ctx, int flags, const double* h_points, int64_t bat
     const int ns = L.gscratch ? 1 : std::min(nchunks, int(pj_ctx::kHostStreams));
     DeviceGuard dg;
     PJ_CUDA(dg.enter(ctx->device));
-    // a stale flag from an earlier asynchronous pj_evaluate must not fail this call
-    PJ_CUDA(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->hstream[0]));
-    PJ_CUDA(cudaStreamSynchronize(ctx->hstream[0]));
+    // a stale flag from an earlier asynchronous pj_evaluate must not fail this call (the small-batch
+    // path below resets it on its own stream)
+    const bool small = size_t(batch) * out_pt <= pj_ctx::kSmallOut && nchunks == 1;
+    if (!small) {
+        PJ_CUDA(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), ctx->hstream[0]));
+        PJ_CUDA(cudaStreamSynchronize(ctx->hstream[0]));
+    }
     if (size_t(chunk) * in_pt > ctx->in_cap || size_t(chunk) * out_pt > ctx->out_cap) {
         for (int i = 0; i < pj_ctx::kHostStreams; ++i) {
             cudaFree(ctx->d_in[i]);
@@ -1491,6 +1516,45 @@ int pj_evaluate_host(pj_ctx* ctx, int flags, const double* h_points, int64_t bat
         }
         ctx->in_cap = size_t(chunk) * in_pt;
         ctx->out_cap = size_t(chunk) * out_pt;
+    }
+    if (small) {
+        // small batch (C1: one point): page-locked staging, everything on one stream — the flag
+        // reset, H2D, the kernel, D2H of the results and of the flag (then its reset) — and one
+        // synchronisation, instead of pageable copies and separate flag round trips
+        const size_t in_b = size_t(batch) * in_pt, out_b = size_t(batch) * out_pt;
+        const size_t in_cap_b = pj_ctx::kSmallOut / out_pt * in_pt;  // points of the largest small batch
+        if (!ctx->h_small) {
+            PJ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_small), in_cap_b + pj_ctx::kSmallOut + 16,
+                                  cudaHostAllocDefault));
+            ctx->h_small_in = in_cap_b;
+        }
+        if (in_b > ctx->h_small_in) {  // (a different precision's point size: grow the staging)
+            cudaFreeHost(ctx->h_small);
+            ctx->h_small = nullptr;
+            PJ_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&ctx->h_small), in_b + pj_ctx::kSmallOut + 16,
+                                  cudaHostAllocDefault));
+            ctx->h_small_in = in_b;
+        }
+        char* hin = ctx->h_small;
+        char* hout = ctx->h_small + ctx->h_small_in;
+        int* hflag = reinterpret_cast<int*>(hout + pj_ctx::kSmallOut);
+        cudaStream_t st = ctx->hstream[0];
+        std::memcpy(hin, h_points, in_b);
+        PJ_CUDA(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), st));
+        PJ_CUDA(cudaMemcpyAsync(ctx->d_in[0], hin, in_b, cudaMemcpyHostToDevice, st));
+        int rc = pj_evaluate(ctx, flags, ctx->d_in[0], batch, ctx->d_out[0], st);
+        if (rc) {
+            cudaStreamSynchronize(st);
+            return rc;
+        }
+        PJ_CUDA(cudaMemcpyAsync(hout, ctx->d_out[0], out_b, cudaMemcpyDeviceToHost, st));
+        PJ_CUDA(cudaMemcpyAsync(hflag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+        PJ_CUDA(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), st));
+        PJ_CUDA(cudaStreamSynchronize(st));
+        if (*hflag) return fail(PJ_ENONFINITE, "evaluate: non-finite coordinate");
+        std::memcpy(h_out, hout, out_b);
+        g_err.clear();
+        return PJ_OK;
     }
     int rc = PJ_OK;
     for (int c = 0; c < nchunks && rc == PJ_OK; ++c) {

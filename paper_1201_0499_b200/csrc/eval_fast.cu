@@ -50,7 +50,7 @@ constexpr int fast_max_threads() { return K <= 12 ? 256 : 512; }
 template <int K, int NS, bool D2>
 __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) fast_kernel(DevSystem S, const double* __restrict__ pts,
                                                    double* __restrict__ out, long long B, int TP,
-                                                   int* __restrict__ flag) {
+                                                   int* __restrict__ flag, int SP) {
     constexpr int W = 4;
     constexpr int R = K + 1;                 // stage-3 schedule entries per lane
     constexpr int stgW = (K + 1) * W * 32;   // staging doubles per warp
@@ -68,7 +68,10 @@ __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) f
     const CDD one = {1.0, 0.0, 0.0, 0.0};
     const CDD zero = {0.0, 0.0, 0.0, 0.0};
 
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    // SP CTAs share each tile (SP > 1 only for batches with fewer tiles than CTAs; the host makes
+    // the grid a multiple of SP): CTA blockIdx takes part blockIdx mod SP of the tile's tasks,
+    // warp + part*nw with step SP*nw, so a single point's 32 rows still spread over the SM array
+    for (long long tile = blockIdx.x / SP; tile < ntiles; tile += gridDim.x / SP) {
         const long long b0 = tile * TP;
         const int tp = (int)min((long long)TP, B - b0);
         for (int i = threadIdx.x; i < tp * n; i += blockDim.x) {
@@ -94,7 +97,7 @@ __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) f
             }
             __syncthreads();
         }
-        for (int task = warp; task < tp * n; task += nw) {
+        for (int task = warp + (int)(blockIdx.x % SP) * nw; task < tp * n; task += nw * SP) {
             const int p = task / tp, t = task - p * tp;
             const double* xt = tab + t * tabPt;
             for (int c = 0; c < C; ++c) {
@@ -359,7 +362,7 @@ cudaError_t launch_t(const LaunchCfg& L, const DevSystem& S, const double* pts, 
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_limit((const void*)kern));
         if (e != cudaSuccess) return e;
     }
-    kern<<<L.blocks, L.threads, L.smem_bytes, st>>>(S, pts, out, B, L.tp, L.flag);
+    kern<<<L.blocks, L.threads, L.smem_bytes, st>>>(S, pts, out, B, L.tp, L.flag, L.splits);
     return cudaGetLastError();
 }
 

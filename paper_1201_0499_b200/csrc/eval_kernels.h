@@ -71,6 +71,8 @@ struct LaunchCfg {
     double* gscratch = nullptr;  // non-null: tables/staging in global memory (huge systems)
     int* flag = nullptr;      // device int, set to 1 on a non-finite coordinate
     int producers = 0;        // warp-specialised dd kernel (variant 3): producer warps per CTA
+    int splits = 1;           // fast dd kernel (variant 1): CTAs sharing one tile's tasks — set per
+                              // launch for batches with fewer tiles than CTAs (pj_evaluate)
 };
 
 cudaError_t launch_eval(int prec, int order, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out,

@@ -444,6 +444,8 @@ class EvaluationContext:
         self._clean = True
         self._zeros = None
         self._layout = None
+        self._per_eval = None  # MultCounter of one evaluation (the tally is linear in the count)
+        self._one_out = None   # staging array of the single-point API
 
     def __del__(self):
         h = getattr(self, "_h", None)
@@ -507,8 +509,14 @@ class EvaluationContext:
         return MultCounter(*[int(v) for v in c])
 
     def _add_tally(self, evals):
-        t = self._tally(evals)
+        # the closed-form counts are linear in the number of evaluations: one C call per context
+        if self._per_eval is None:
+            self._per_eval = self._tally(1)
+        t = self._per_eval
         mc = self._mults
+        if evals != 1:
+            t = MultCounter(*[evals * getattr(t, f) for f in ("stage1_powers", "stage1_factors", "stage2",
+                                                              "speelpenning", "stage3")])
         mc.stage1_powers += t.stage1_powers
         mc.stage1_factors += t.stage1_factors
         mc.stage2 += t.stage2
@@ -537,16 +545,17 @@ class EvaluationContext:
     def evaluate(self, point) -> EvaluationResult:
         """One point (sequence of n complex numbers) in complex double; bit-identical with the
         reference's EvaluationContext::evaluate."""
-        z = np.asarray(point, np.complex128).reshape(-1)
+        z = np.ascontiguousarray(point, np.complex128).reshape(-1)
         if z.shape[0] != self.n:
             raise ValueError("evaluate: point dimension mismatch")
-        if not np.all(np.isfinite(z.real) & np.isfinite(z.imag)):
+        pts = z.view(np.float64).reshape(1, self.n, 2)  # complex128 is (re, im) interleaved already
+        if not np.isfinite(pts).all():
             raise ValueError("evaluate: non-finite coordinate")
-        pts = np.stack([z.real, z.imag], -1)[None]
-        out = self.evaluate_host(pts, "d")
+        if self._one_out is None:  # results are copied out below: one staging array per context
+            self._one_out = np.empty((1, self.n + self.n * self.n, 2), np.float64)
+        out = self.evaluate_host(pts, "d", out=self._one_out)
         self._audit(out)
-        out = out[0]
-        c = out[:, 0] + 1j * out[:, 1]
+        c = out[0].view(np.complex128)[:, 0]
         return EvaluationResult(self.n, c[: self.n].copy(), c[self.n:].copy())
 
     def evaluate_dd(self, points_dd: np.ndarray, order: str | None = None) -> np.ndarray:
