@@ -1482,11 +1482,14 @@ int pj_evaluate_host(pj_ctx* ctx, int flags, const double* h_points, int64_t bat
     const int W = pi == 0 ? 2 : 4;
     const size_t in_pt = size_t(ctx->n) * W * 8;
     const size_t out_pt = (size_t(ctx->n) * ctx->n + ctx->n) * W * 8;
-    // chunk: large enough to fill every SM for several waves, small enough that the D2H of
-    // one chunk overlaps the kernel of the next (pinned host buffers give full overlap)
+    // chunk: at least one full wave of the kernel, small enough that the D2H of one chunk
+    // overlaps the kernel of the next (pinned host buffers give full overlap)
     const pjb::LaunchCfg& L = ctx->mode[mode_of(flags)].cfg;
-    int64_t chunk = std::max<int64_t>(int64_t(L.blocks) * L.tp * 4, 1024);
-    chunk = std::max<int64_t>(chunk, int64_t((256ull << 20) / out_pt));
+    // (measured at C2 with pinned buffers, tools/pcie_bw.py + profiles/r02_e2e_chunks.log: one wave
+    // and >= 64 MiB of results per chunk reach 56.3 GB/s of results, the box's D2H ceiling is
+    // 56.5; four waves / 256 MiB chunks 55.5 — the pipeline fill and drain are a chunk each)
+    int64_t chunk = std::max<int64_t>(int64_t(L.blocks) * L.tp, 1024);
+    chunk = std::max<int64_t>(chunk, int64_t((size_t(64) << 20) / out_pt));
     // bounded staging: at most ~1 GiB of results per stream (wide systems have MB-sized results)
     chunk = std::min<int64_t>(chunk, std::max<int64_t>(1, int64_t((1ull << 30) / out_pt)));
     chunk = std::min<int64_t>(chunk, batch);

@@ -423,3 +423,25 @@ def test_distinct_contexts_are_thread_safe(gpu):
     for t in th:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("shape", [(32, 32, 8, 2), (64, 64, 16, 10)], ids=["C2", "C3"])
+def test_small_batches_split_tiles_bit_identical(shape, gpu):
+    """Batches with fewer tiles than CTAs spread each tile's tasks over several CTAs (pj_evaluate,
+    eval_fast.cu SP): the arithmetic of a task does not depend on who runs it, so every point's
+    results are bit-identical whether it is evaluated alone, in a small batch or in a full one,
+    and they stay within the contract of the oracle."""
+    n, m, k, d = shape
+    s = pj.random_system(n, m, k, d, 7)
+    ctx = pj.EvaluationContext(s)
+    S = sysd_of(s)
+    B = 2000
+    p4 = stress_dd(pj.random_points(n, B, 5), seed=3)
+    full = ctx.evaluate_dd(p4)
+    for b in [1, 2, 3, 7, 100]:
+        got = ctx.evaluate_dd(p4[:b])
+        assert np.array_equal(got.view(np.uint64), full[:b].view(np.uint64)), b
+    got1 = ctx.evaluate_dd(p4[B - 1:])
+    assert np.array_equal(got1.view(np.uint64), full[B - 1:].view(np.uint64))
+    want, ms = O.evaluate("dd", S, p4[:7], magsum=True)
+    assert dd_rel(full[:7], want, ms) <= DD_TOL
