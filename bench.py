@@ -629,6 +629,15 @@ def main():
                           "e2e_api": "EvaluationContext.newton_host -> pj_newton_host (H2D points, evaluate + solve "
                                      "in L2-sized chunks, D2H corrected points, norms, status)",
                           "launch": ctx.launch("dd", newton=True)}
+        # the mixed-precision solve (PJ_NEWTON_MIXED, opt-in): complex-double factors of the dd
+        # Jacobian, two dd-residual refinement steps; dd points in and out, status 3 when the
+        # refinement has not converged (then the dd solve above is the one to use)
+        ms_solve_mx = timed(lambda: ctx.newton_solve_device(out_x, x_dd, xo, "mixed", status=nst, stream=stream), 5)
+        ms_step_mx = timed(lambda: ctx.newton_step_device(x_dd, out_x, xo, "mixed", status=nst, stream=stream), 5)
+        line["newton"]["mixed"] = {"solve_ms": ms_solve_mx, "solve_points_per_s": Bx / (ms_solve_mx * 1e-3),
+                                   "steps_per_s": Bx / (ms_step_mx * 1e-3), "ms_per_step": ms_step_mx,
+                                   "status_ok_frac": float((nst == 0).float().mean().item()),
+                                   "launch": ctx.launch("mixed", newton=True)}
         del xo, x_dd
         # C1: one point through the reference-shaped host API (EvaluationContext.evaluate:
         # H2D, kernel, D2H, unpack), complex double as the reference; and one dd point

@@ -46,6 +46,10 @@ extern "C" {
                                oracle's dd restatement); default dd order is the fast one */
 #define PJ_ORDER_FAST 0x20  /* d: allow the fast order (default for d is the reference order) */
 #define PJ_OP_NEWTON 0x100  /* pj_set_launch / pj_get_launch: address the Newton solve kernel */
+#define PJ_NEWTON_MIXED 0x400 /* pj_newton_solve / _step / _host with PJ_PREC_DD, n <= 32: factor J in
+                                 complex double (its high words), then two steps of iterative refinement
+                                 with complex-dd residuals; status 3 when the refinement has not
+                                 converged (J too ill-conditioned for double factors: use the dd solve) */
 #define PJ_VALIDATE 0x200   /* pj_evaluate: check every coordinate first and return PJ_ENONFINITE
                                without writing any output when one is non-finite (the
                                reference's throw-before-evaluate, ref src/engine.cpp:183-188);

@@ -517,6 +517,109 @@ void newton_one(int n, const double* ev, const double* x, const double* y, doubl
     if (status) *status = fin ? 0 : 2;
 }
 
+// Mixed-precision solve (PJ_NEWTON_MIXED; csrc/newton.cu: nt_load_mixed / nt_mixed_finish):
+// complex-double elimination of the high words of J and rhs (newton_one<NT_D>'s operation order),
+// then kIters steps of iterative refinement with complex-dd residuals summed in four interleaved
+// column groups, each correction solved with the double factors.
+void newton_one_mixed(int n, const double* ev, const double* x, const double* y, double* xo, double* norms,
+                      int* status) {
+    using OD = Ops<CD>;
+    using OQ = Ops<CDD>;
+    constexpr int kIters = 2;
+    const int ld = n + 1;
+    auto J = [&](int i, int j) { return OQ::load(ev + size_t(n + i * n + j) * 4); };
+    std::vector<CD> A(size_t(n) * ld), inv(n);
+    std::vector<CDD> rhs(n);
+    double rn = 0.0;
+    for (int i = 0; i < n; ++i) {
+        for (int j = 0; j < n; ++j) {
+            const CDD v = J(i, j);
+            A[size_t(i) * ld + j] = CD{v.rh, v.ih};
+        }
+        CDD r = NT_DD::neg(OQ::load(ev + size_t(i) * 4));
+        if (y) r = OQ::add(OQ::load(y + size_t(i) * 4), r);
+        rhs[i] = r;
+        A[size_t(i) * ld + n] = CD{r.rh, r.ih};
+        rn = std::fmax(rn, NT_DD::magmax(r));
+    }
+    if (norms) norms[0] = rn;
+    auto at = [&](int i, int j) -> CD& { return A[size_t(i) * ld + j]; };
+    std::vector<int> piv(n), step(n, n);
+    for (int kk = 0; kk < n; ++kk) {
+        double best = 0.0;
+        int bi = -1;
+        for (int i = 0; i < n; ++i) {
+            if (step[i] < kk) continue;
+            const double mg = NT_D::mag1(at(i, kk));
+            if (mg > best) {
+                best = mg;
+                bi = i;
+            }
+        }
+        if (bi < 0) {
+            for (int i = 0; i < n; ++i) OQ::store(xo + size_t(i) * 4, OQ::load(x + size_t(i) * 4));
+            if (norms) norms[1] = INFINITY;
+            if (status) *status = 1;
+            return;
+        }
+        piv[kk] = bi;
+        step[bi] = kk;
+        inv[kk] = NT_D::inv(at(bi, kk));
+        for (int i = 0; i < n; ++i) {
+            if (step[i] <= kk) continue;
+            const CD l = OD::mul(at(i, kk), inv[kk]);
+            at(i, kk) = l;
+            for (int j = kk + 1; j <= n; ++j) at(i, j) = OD::add(at(i, j), NT_D::neg(NT_D::umul(l, at(bi, j))));
+        }
+    }
+    // triangular solves with the double factors on b (physical rows), in the kernel's order
+    std::vector<CD> b(n), c(n);
+    auto back = [&]() {
+        for (int s = n - 1; s >= 0; --s) {
+            c[s] = OD::mul(b[piv[s]], inv[s]);
+            for (int t = 0; t < n; ++t)
+                if (step[t] < s) b[t] = OD::add(b[t], NT_D::neg(NT_D::umul(at(t, s), c[s])));
+        }
+    };
+    for (int i = 0; i < n; ++i) b[i] = at(i, n);
+    back();
+    std::vector<CDD> dx(n);
+    for (int i = 0; i < n; ++i) dx[i] = CDD{c[i].re, 0.0, c[i].im, 0.0};
+    double cmax = 0.0;
+    for (int it = 0; it < kIters; ++it) {
+        for (int i = 0; i < n; ++i) {
+            CDD acc[4];
+            for (int g = 0; g < 4; ++g) {
+                acc[g] = CDD{0.0, 0.0, 0.0, 0.0};
+                for (int j = g; j < n; j += 4) acc[g] = OQ::add(acc[g], NT_DD::umul(J(i, j), dx[j]));
+            }
+            const CDD r = OQ::add(rhs[i], NT_DD::neg(OQ::add(OQ::add(acc[0], acc[1]), OQ::add(acc[2], acc[3]))));
+            b[i] = CD{r.rh, r.ih};
+        }
+        for (int kk = 0; kk < n; ++kk) {
+            const CD bp = b[piv[kk]];
+            for (int i = 0; i < n; ++i)
+                if (step[i] > kk) b[i] = OD::add(b[i], NT_D::neg(NT_D::umul(at(i, kk), bp)));
+        }
+        back();
+        cmax = 0.0;
+        for (int i = 0; i < n; ++i) {
+            dx[i] = OQ::add(dx[i], CDD{c[i].re, 0.0, c[i].im, 0.0});
+            cmax = std::fmax(cmax, NT_D::magmax(c[i]));
+        }
+    }
+    double dn = 0.0;
+    bool fin = true;
+    for (int i = 0; i < n; ++i) {
+        const CDD xn = OQ::add(OQ::load(x + size_t(i) * 4), dx[i]);
+        OQ::store(xo + size_t(i) * 4, xn);
+        dn = std::fmax(dn, NT_DD::magmax(dx[i]));
+        fin = fin && NT_DD::finite(xn);
+    }
+    if (norms) norms[1] = dn;
+    if (status) *status = !fin ? 2 : (cmax > std::ldexp(dn, -64) ? 3 : 0);
+}
+
 }  // namespace oracle
 
 extern "C" {
@@ -652,7 +755,8 @@ long long oracle_zero_mask(int n, int m, int k, const int* pos, long long* mask)
 // [B][n][W] (target nullable), norms [B][2] and status [B] nullable.
 int oracle_newton_solve(int prec, int n, const double* evals, const double* points, const double* target, long B,
                         double* out, double* norms, int* status, int threads) {
-    if (prec != 1 && prec != 2) return 1;
+    if (prec != 1 && prec != 2 && prec != 3) return 1;  // 3: the mixed solve (dd input)
+    if (prec == 3 && n > 32) return 1;
     const int W = prec == 1 ? 2 : 4;
     const size_t nout = size_t(n) * n + n;
     if (threads < 1) threads = 1;
@@ -668,6 +772,8 @@ int oracle_newton_solve(int prec, int n, const double* evals, const double* poin
             int* st = status ? status + b : nullptr;
             if (prec == 1)
                 oracle::newton_one<oracle::NT_D>(n, ev, x, y, xo, nr, st);
+            else if (prec == 3)
+                oracle::newton_one_mixed(n, ev, x, y, xo, nr, st);
             else
                 oracle::newton_one<oracle::NT_DD>(n, ev, x, y, xo, nr, st);
         }

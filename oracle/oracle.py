@@ -168,7 +168,8 @@ def evaluate_ragged(prec, rsys, points, threads=1, magsum=False):
 
 def newton_solve(prec, n, evals, points, target=None, threads=1):
     """CPU restatement of the Newton corrector (paper_1201_0499_b200/csrc/newton.cu): per point
-    solve J dx = y - f from the evaluator's output and return (x + dx, norms [B, 2], status [B])."""
+    solve J dx = y - f from the evaluator's output and return (x + dx, norms [B, 2], status [B]).
+    prec: "d", "dd", or "mixed" (dd input; complex-double factors + dd iterative refinement)."""
     W = 2 if prec == "d" else 4
     ev = np.ascontiguousarray(evals, np.float64)
     pts = np.ascontiguousarray(points, np.float64)
@@ -181,7 +182,7 @@ def newton_solve(prec, n, evals, points, target=None, threads=1):
     out = np.empty_like(pts)
     norms = np.empty((B, 2), np.float64)
     status = np.empty(B, np.int32)
-    rc = lib().oracle_newton_solve(1 if prec == "d" else 2, n, ev, pts, tg.ctypes.data if tg is not None else None,
+    rc = lib().oracle_newton_solve({"d": 1, "dd": 2, "mixed": 3}[prec], n, ev, pts, tg.ctypes.data if tg is not None else None,
                                    B, out, norms.ctypes.data, status.ctypes.data, threads)
     if rc:
         raise RuntimeError("oracle_newton_solve failed")

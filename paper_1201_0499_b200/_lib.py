@@ -16,6 +16,7 @@ PJ_OK, PJ_EINVAL, PJ_ERANGE, PJ_ECUDA, PJ_ENOMEM, PJ_ENONFINITE, PJ_EFORMAT = 0,
 PJ_PREC_D, PJ_PREC_DD = 1, 2
 PJ_ORDER_REF, PJ_ORDER_FAST = 0x10, 0x20
 PJ_OP_NEWTON = 0x100
+PJ_NEWTON_MIXED = 0x400
 PJ_VALIDATE = 0x200
 PJ_CTX_WIDE = 0x1
 

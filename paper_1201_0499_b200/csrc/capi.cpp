@@ -456,7 +456,7 @@ struct pj_ctx {
         bool panel = false;
         size_t smem = 0;
         bool gscr = false;
-    } newton[2];
+    } newton[3];  // complex double, complex dd, mixed (PJ_NEWTON_MIXED)
     double* d_nscratch = nullptr;
     size_t nscratch_bytes = 0;
     double *d_nx[kHostStreams] = {}, *d_nwork[kHostStreams] = {}, *d_ntgt[kHostStreams] = {},
@@ -697,6 +697,12 @@ int check_desc(const pj_system_desc* sys, bool wide) {
 
 // ------------------------------------------------------------------ Newton corrector (f1)
 namespace {
+// Newton plan index: 0 complex double, 1 complex dd, 2 the mixed solve (PJ_NEWTON_MIXED with
+// PJ_PREC_DD: complex-double factors, dd refinement); its kernel precision code is index + 1
+int newton_index(int flags) {
+    const int p = flags & 0x0f;
+    return p == PJ_PREC_D ? 0 : p == PJ_PREC_DD ? ((flags & PJ_NEWTON_MIXED) ? 2 : 1) : -1;
+}
 int newton_plan(pj_ctx* c, int pi, pj_ctx::NewtonPlan** out) {
     pj_ctx::NewtonPlan& P = c->newton[pi];
     const int prec = pi + 1;
@@ -705,8 +711,9 @@ int newton_plan(pj_ctx* c, int pi, pj_ctx::NewtonPlan** out) {
         // n <= 32: 128-thread CTAs (the kernel is compiled for at most 128 there, newton.cu)
         P.threads = P.over_threads ? P.over_threads : pjb::newton_max_threads(c->n);
         P.threads = std::min(P.threads, pjb::newton_max_threads(c->n));
+        if (pi == 2) P.threads = 128;  // the mixed solve's residual uses exactly four warps
         // the panel kernel is opt-in: measured slower at C2 (dd 10.7 vs 7.2 ms, d 2.50 vs 2.44 ms)
-        P.panel = pjb::newton_panel_supported(c->n) && P.over_variant == 1 && mb + ib <= c->smem_optin;
+        P.panel = pi < 2 && pjb::newton_panel_supported(c->n) && P.over_variant == 1 && mb + ib <= c->smem_optin;
         if (P.panel) P.threads = std::max(P.threads, 64);  // one look-ahead warp + updaters
         if (mb + ib <= c->smem_optin) {
             const int nb = pjb::newton_blocks_per_sm(prec, c->n, P.threads, mb + ib, P.panel, false);
@@ -1871,8 +1878,8 @@ int pj_set_launch(pj_ctx* ctx, int flags, int threads, int tile_points) {
     if (tile_points < 0) return fail(PJ_EINVAL, "tile_points must be >= 0");
     if (flags & PJ_OP_NEWTON) {
         if (threads == 32) return fail(PJ_EINVAL, "newton: threads must be >= 64");
-        ctx->newton[pi].over_threads = threads;
-        ctx->newton[pi].blocks = 0;  // re-planned on the next solve
+        ctx->newton[newton_index(flags)].over_threads = threads;
+        ctx->newton[newton_index(flags)].blocks = 0;  // re-planned on the next solve
         g_err.clear();
         return PJ_OK;
     }
@@ -1906,8 +1913,8 @@ int pj_set_kernel_variant(pj_ctx* ctx, int flags, int variant) {
         if (variant > 1 || variant < -1) return fail(PJ_EINVAL, "unknown kernel variant");
         if (variant == 1 && !pjb::newton_panel_supported(ctx->n))
             return fail(PJ_EINVAL, "newton: the panel kernel needs n <= 32");
-        ctx->newton[pi].over_variant = variant;
-        ctx->newton[pi].blocks = 0;  // re-planned on the next solve
+        ctx->newton[newton_index(flags)].over_variant = variant;
+        ctx->newton[newton_index(flags)].blocks = 0;  // re-planned on the next solve
         g_err.clear();
         return PJ_OK;
     }
@@ -1942,7 +1949,7 @@ int pj_get_launch(pj_ctx* ctx, int flags, int32_t* threads, int32_t* tile_points
         cudaGetDevice(&prev);
         cudaSetDevice(ctx->device);
         pj_ctx::NewtonPlan* P = nullptr;
-        int rc = newton_plan(ctx, pi, &P);
+        int rc = newton_plan(ctx, newton_index(flags), &P);
         cudaSetDevice(prev);
         if (rc) return rc;
         if (threads) *threads = P->threads;
@@ -1978,11 +1985,13 @@ int pj_newton_solve(pj_ctx* ctx, int flags, const double* d_evals, const double*
     if (!d_evals || !d_points || !d_points_out) return fail(PJ_EINVAL, "newton: null buffer");
     if (ctx->host_only) return fail(PJ_EINVAL, "newton: host-only context (created with device < 0)");
     if (ctx->n > 256) return fail(PJ_EINVAL, "newton: n > 256 is not supported");
+    const int ni = newton_index(flags);
+    if (ni == 2 && ctx->n > 32) return fail(PJ_EINVAL, "newton: the mixed solve (PJ_NEWTON_MIXED) needs n <= 32");
     int prev = 0;
     cudaGetDevice(&prev);
     if (prev != ctx->device) PJ_CUDA(cudaSetDevice(ctx->device));
     pj_ctx::NewtonPlan* P = nullptr;
-    int rc = newton_plan(ctx, pi, &P);
+    int rc = newton_plan(ctx, ni, &P);
     if (rc) {
         if (prev != ctx->device) cudaSetDevice(prev);
         return rc;
@@ -1997,8 +2006,8 @@ int pj_newton_solve(pj_ctx* ctx, int flags, const double* d_evals, const double*
     a.norms = d_norms;
     a.status = d_status;
     a.gscratch = P->gscr ? ctx->d_nscratch : nullptr;
-    a.gstride = (pjb::newton_matrix_bytes(pi + 1, ctx->n) / sizeof(double) + 31) / 32 * 32;
-    cudaError_t e = pjb::launch_newton(pi + 1, a, P->blocks, P->threads, P->smem, P->panel, (cudaStream_t)stream);
+    a.gstride = (pjb::newton_matrix_bytes(ni + 1, ctx->n) / sizeof(double) + 31) / 32 * 32;
+    cudaError_t e = pjb::launch_newton(ni + 1, a, P->blocks, P->threads, P->smem, P->panel, (cudaStream_t)stream);
     if (prev != ctx->device) cudaSetDevice(prev);
     if (e) return cuda_fail(e, "newton: kernel launch");
     g_err.clear();
@@ -2040,7 +2049,7 @@ int pj_newton_step(pj_ctx* ctx, int flags, const double* d_points, const double*
         DeviceGuard dg;
         PJ_CUDA(dg.enter(ctx->device));
         pj_ctx::NewtonPlan* P = nullptr;
-        const int prc = newton_plan(ctx, pi, &P);
+        const int prc = newton_plan(ctx, newton_index(flags), &P);
         if (prc) return prc;
         gslab = gslab || P->gscr;
     }
@@ -2104,7 +2113,7 @@ int pj_newton_host(pj_ctx* ctx, int flags, const double* h_points, const double*
     DeviceGuard dg;
     PJ_CUDA(dg.enter(ctx->device));
     pj_ctx::NewtonPlan* P = nullptr;
-    rc0 = newton_plan(ctx, pi, &P);
+    rc0 = newton_plan(ctx, newton_index(flags), &P);
     if (rc0) return rc0;
     // global-scratch slabs (evaluation tables or Newton matrices beyond shared memory) are indexed
     // by CTA: such launches must not overlap, so the chunks then run on one stream

@@ -265,6 +265,178 @@ __device__ __forceinline__ void nt_back_substitute(const NewtonArgs& a, long lon
     }
 }
 
+// ---- mixed-precision solve (PJ_NEWTON_MIXED, complex dd input, n <= 32): the LU factorisation in
+// complex double on the high words of J, then NIT steps of iterative refinement with the residual
+// in complex dd. Operation order (restated by oracle/oracle.cpp: newton_one_mixed):
+//   rhs = y + (-f) in dd (-f when y is absent); A = (Re hi, Im hi) of J, column n = hi words of rhs;
+//   the complex-double elimination of newton_kernel<CD> on [A | rhs_hi]; dx = its back substitution
+//   (in dd with zero low words); then NIT times:
+//     partial residuals per row i and group g = 0..3: acc_g = sum over j = g, g+4, ... ascending of
+//       cdd_mul_u(J_ij, dx_j) (cdd_add, starting from 0); r_i = rhs_i + (-((acc_0 + acc_1) + (acc_2 + acc_3)));
+//     b = hi words of r; forward substitution with the stored multipliers (step order, the same
+//     operations the elimination applied to the right-hand side column); back substitution with
+//     the pivot inverses -> c (complex double); dx_j = dx_j + c_j (dd add, c's low words zero);
+//   x_new = x + dx (dd). status 3 when the last correction is not below 2^-64 of |dx| (the
+//   refinement has not converged to dd accuracy: J too ill-conditioned for the double factors).
+constexpr int kMixedIters = 2;
+
+__device__ __forceinline__ void nt_load_mixed(const NewtonArgs& a, long long b, double* A, int* list, int* sing,
+                                              int warp) {
+    const int n = a.n, ld = n + 1, P = n * ld;
+    const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31;
+    const double* ev = a.evals + size_t(b) * (size_t(n) * n + n) * 4;
+    // the high words (re_hi, im_hi) of every J element into the complex-double pair layout
+    const int es = nt / 2, di = es / n, dj = es - di * n;
+    int el = tid / 2;
+    const int comp = tid - el * 2;
+    int i = el / n, j = el - i * n;
+    for (int t = tid; t < n * n * 2; t += nt) {
+        const unsigned dst = unsigned(__cvta_generic_to_shared(A + NL<CD>::off(i * ld + j, comp, P)));
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(dst), "l"(ev + size_t(n) * 4 + 2 * t));
+        i += di;
+        j += dj;
+        if (j >= n) {
+            j -= n;
+            ++i;
+        }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    if (warp == 0) {
+        double rn = 0.0;
+        for (int r = lane; r < n; r += 32) {
+            CDD v = nt_neg(Sc<CDD>::ld_aos(ev + size_t(r) * 4));
+            if (a.target) v = cdd_add(Sc<CDD>::ld_aos(a.target + (size_t(b) * n + r) * 4), v);
+            NL<CD>::st(A, r * ld + n, P, CD{v.rh, v.ih});
+            rn = fmax(rn, nt_magmax(v));
+            list[r] = r;
+        }
+        for (int o = 16; o; o >>= 1) rn = fmax(rn, __shfl_xor_sync(0xffffffffu, rn, o));
+        if (lane == 0) {
+            if (a.norms) a.norms[2 * b] = rn;
+            *sing = 0;
+        }
+    }
+}
+
+// After the complex-double elimination (all threads; n <= 32, lanes = physical rows). DXD: the dd
+// solution [4][n] (pair layout), PART: four dd partial residuals per row [4][4n], DXC: corrections.
+__device__ __forceinline__ void nt_mixed_finish(const NewtonArgs& a, long long b, const double* A, const double* INV,
+                                                double* DXD, double* PART, double* DXC, const int* s_piv,
+                                                const int* s_step, bool singular, int warp) {
+    const int n = a.n, ld = n + 1, P = n * ld, lane = threadIdx.x & 31;
+    const double* x = a.points + size_t(b) * n * 4;
+    double* xo = a.points_out + size_t(b) * n * 4;
+    const double* ev = a.evals + size_t(b) * (size_t(n) * n + n) * 4;
+    if (singular) {
+        if (warp == 0) {
+            for (int i = lane; i < n; i += 32) Sc<CDD>::st_aos(xo + size_t(i) * 4, Sc<CDD>::ld_aos(x + size_t(i) * 4));
+            if (lane == 0) {
+                if (a.norms) a.norms[2 * b + 1] = INFINITY;
+                if (a.status) a.status[b] = 1;
+            }
+        }
+        return;
+    }
+    const bool row = lane < n;
+    const int st = row ? s_step[lane] : -1;  // the step this lane's physical row was pivoted at
+    // complex-double triangular solves on the lane-held right-hand side b (physical rows): the
+    // forward substitution repeats the elimination's updates of column n, then the back substitution
+    // (each step's pivot row, inverse and matrix entry are loaded one step ahead: off the chain)
+    auto back = [&](CD bb) {
+        int pr = s_piv[n - 1];
+        CD iv = NL<CD>::ld(INV, n - 1, n), av = row ? NL<CD>::ld(A, lane * ld + n - 1, P) : CD{0.0, 0.0};
+        for (int s = n - 1; s >= 0; --s) {
+            const int s1 = s > 0 ? s - 1 : 0;
+            const int pr1 = s_piv[s1];
+            const CD iv1 = NL<CD>::ld(INV, s1, n);
+            const CD av1 = row ? NL<CD>::ld(A, lane * ld + s1, P) : CD{0.0, 0.0};
+            CD xs = shfl_idx(bb, pr);
+            xs = cd_mul(xs, iv);
+            if (lane == 0) NL<CD>::st(DXC, s, n, xs);
+            if (row && st < s) bb = cd_add(bb, nt_neg(cd_mul(av, xs)));
+            pr = pr1;
+            iv = iv1;
+            av = av1;
+        }
+        __syncwarp();
+    };
+    double cmax = 0.0;
+    CDD rhs{0.0, 0.0, 0.0, 0.0};  // warp 0: this lane's dd right-hand side, kept for the residuals
+    if (warp == 0 && row) {
+        rhs = nt_neg(Sc<CDD>::ld_aos(ev + size_t(lane) * 4));
+        if (a.target) rhs = cdd_add(Sc<CDD>::ld_aos(a.target + (size_t(b) * n + lane) * 4), rhs);
+    }
+    if (warp == 0) {
+        back(row ? NL<CD>::ld(A, lane * ld + n, P) : CD{0.0, 0.0});
+        for (int i = lane; i < n; i += 32) {
+            const CD c = NL<CD>::ld(DXC, i, n);
+            NL<CDD>::st(DXD, i, n, CDD{c.re, 0.0, c.im, 0.0});
+        }
+    }
+    for (int it = 0; it < kMixedIters; ++it) {
+        __syncthreads();  // DXD complete
+        // partial residual sums: warp g, lane = row i, columns j = g, g+4, ...
+        if (row) {
+            CDD acc{0.0, 0.0, 0.0, 0.0};
+            const double* jr = ev + (size_t(n) + size_t(lane) * n) * 4;
+            for (int j = warp; j < n; j += 4)
+                acc = cdd_add(acc, cdd_mul_u(Sc<CDD>::ld_aos(jr + size_t(j) * 4), NL<CDD>::ld(DXD, j, n)));
+            NL<CDD>::st(PART + warp * 4 * n, lane, n, acc);
+        }
+        __syncthreads();
+        if (warp == 0) {
+            CD bb{0.0, 0.0};
+            CDD r{0.0, 0.0, 0.0, 0.0};
+            if (row) {
+                r = rhs;
+                const CDD s01 = cdd_add(NL<CDD>::ld(PART, lane, n), NL<CDD>::ld(PART + 4 * n, lane, n));
+                const CDD s23 = cdd_add(NL<CDD>::ld(PART + 8 * n, lane, n), NL<CDD>::ld(PART + 12 * n, lane, n));
+                r = cdd_add(r, nt_neg(cdd_add(s01, s23)));
+                bb = CD{r.rh, r.ih};
+            }
+            // forward substitution (the elimination's operations on column n, in step order)
+            int pk = s_piv[0];
+            CD lk = row ? NL<CD>::ld(A, lane * ld, P) : CD{0.0, 0.0};
+            for (int kk = 0; kk < n; ++kk) {
+                const int k1 = kk + 1 < n ? kk + 1 : kk;
+                const int pk1 = s_piv[k1];
+                const CD lk1 = row ? NL<CD>::ld(A, lane * ld + k1, P) : CD{0.0, 0.0};
+                const CD bp = shfl_idx(bb, pk);
+                if (row && st > kk) bb = cd_add(bb, nt_neg(cd_mul(lk, bp)));
+                pk = pk1;
+                lk = lk1;
+            }
+            back(bb);
+            double cm = 0.0;
+            for (int i = lane; i < n; i += 32) {
+                const CD c = NL<CD>::ld(DXC, i, n);
+                NL<CDD>::st(DXD, i, n, cdd_add(NL<CDD>::ld(DXD, i, n), CDD{c.re, 0.0, c.im, 0.0}));
+                cm = fmax(cm, nt_magmax(c));
+            }
+            for (int o = 16; o; o >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
+            cmax = cm;
+        }
+    }
+    if (warp == 0) {
+        __syncwarp();
+        double dn = 0.0;
+        bool fin = true;
+        for (int i = lane; i < n; i += 32) {
+            const CDD d = NL<CDD>::ld(DXD, i, n);
+            const CDD xn = cdd_add(Sc<CDD>::ld_aos(x + size_t(i) * 4), d);
+            Sc<CDD>::st_aos(xo + size_t(i) * 4, xn);
+            dn = fmax(dn, nt_magmax(d));
+            fin = fin && nt_finite(xn);
+        }
+        for (int o = 16; o; o >>= 1) dn = fmax(dn, __shfl_xor_sync(0xffffffffu, dn, o));
+        fin = __all_sync(0xffffffffu, fin);
+        if (lane == 0) {
+            if (a.norms) a.norms[2 * b + 1] = dn;
+            if (a.status) a.status[b] = !fin ? 2 : (cmax > ldexp(dn, -64) ? 3 : 0);
+        }
+    }
+}
+
 // NQ: active-row slots per lane (look-ahead) and rows per lane (back substitution), n <= 32*NQ
 // kRecip[c] = ceil(2^16 / c): floor(x / c) == (x * kRecip[c]) >> 16 for x, c <= 256
 __constant__ unsigned kRecip[257];
@@ -292,13 +464,20 @@ struct NtBounds {
 #endif
 // complex double at n <= 32 (18 KB of matrix): eight CTAs per SM, 64 registers (measured 2.35 ms vs
 // 2.45 (7) and 2.60 (6) at C2)
-template <class T, int NQ>
-constexpr int nt_min_blocks() { return NQ == 1 && Sc<T>::W == 2 ? PJB_NT_MINB_D : NtBounds<NQ>::blocks; }
+#ifndef PJB_NT_MINB_MX
+#define PJB_NT_MINB_MX 8
+#endif
+template <class T, int NQ, bool MX = false>
+constexpr int nt_min_blocks() {
+    return MX ? PJB_NT_MINB_MX : NQ == 1 && Sc<T>::W == 2 ? PJB_NT_MINB_D : NtBounds<NQ>::blocks;
+}
 // GS: the matrix lives in a per-CTA global slab (a.gscratch) instead of shared memory. A separate
 // instantiation, so that in the shared-memory kernel the compiler sees every matrix access as a
 // shared-memory access (LDS/STS, not generic LD/ST that must resolve the address space at run time)
-template <class T, int NQ, bool GS>
-__global__ void __launch_bounds__(NtBounds<NQ>::threads, nt_min_blocks<T, NQ>()) newton_kernel(NewtonArgs a) {
+// MX: the mixed-precision solve (T = CD, NQ = 1: complex-double factorisation of a complex-dd
+// system, refined in dd; see nt_mixed_finish)
+template <class T, int NQ, bool GS, bool MX = false>
+__global__ void __launch_bounds__(NtBounds<NQ>::threads, nt_min_blocks<T, NQ, MX>()) newton_kernel(NewtonArgs a) {
     using S = Sc<T>;
     constexpr int W = S::W;
     extern __shared__ __align__(16) double smem[];
@@ -328,6 +507,9 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, nt_min_blocks<T, NQ>())
     double* A = GS ? a.gscratch + size_t(blockIdx.x) * a.gstride : smem + newton_int_words(n);
     double* INV = A + size_t(W) * P;  // [W][n] pivot inverses
     double* DX = INV + size_t(W) * n;   // [W][n] solution
+    double* DXD = DX + size_t(W) * n;   // MX: the dd solution [4][n], then four partial residuals, corrections
+    double* PART = DXD + 4 * size_t(n);
+    double* DXC = PART + 16 * size_t(n);
 
 #ifdef PJB_NT_TRACE
     long long* tsub = nullptr;  // look-ahead sub-phase clocks (developer instrumentation)
@@ -413,7 +595,10 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, nt_min_blocks<T, NQ>())
 #define PJB_PH(i)
 #endif
     for (long long b = blockIdx.x; b < a.B; b += gridDim.x) {
-        nt_load<T, GS>(a, b, A, s_list0, &s_sing, warp);
+        if constexpr (MX)
+            nt_load_mixed(a, b, A, s_list0, &s_sing, warp);
+        else
+            nt_load<T, GS>(a, b, A, s_list0, &s_sing, warp);
         asm volatile("cp.async.wait_all;\n" ::);
         __syncthreads();
         PJB_PH(0)
@@ -534,7 +719,10 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, nt_min_blocks<T, NQ>())
         }
 
         PJB_PH(1)
-        if (warp == 0) nt_back_substitute<T, NQ>(a, b, A, INV, DX, s_piv, s_step, singular);
+        if constexpr (MX)
+            nt_mixed_finish(a, b, A, INV, DXD, PART, DXC, s_piv, s_step, singular, warp);
+        else if (warp == 0)
+            nt_back_substitute<T, NQ>(a, b, A, INV, DX, s_piv, s_step, singular);
         __syncthreads();  // the next point reuses the matrix storage
         PJB_PH(2)
 #ifdef PJB_NT_PHASES
@@ -753,15 +941,19 @@ const void* newton_fn(int nq, bool gs) {
 // (a global-slab launch with n <= 64 runs the NQ = 4 instantiation: same code, more row slots)
 int nq_of(int n) { return n <= 32 ? 1 : n <= 64 ? 2 : n <= 128 ? 4 : 8; }
 const void* fn_of(int prec, int n, bool panel, bool gs) {
+    if (prec == 3) return (const void*)newton_kernel<CD, 1, false, true>;  // mixed (n <= 32)
     if (panel && !gs) return prec == 1 ? (const void*)newton_panel_kernel<CD> : (const void*)newton_panel_kernel<CDD>;
     return prec == 1 ? newton_fn<CD>(nq_of(n), gs) : newton_fn<CDD>(nq_of(n), gs);
 }
 
 }  // namespace
 
+// prec: 1 complex double, 2 complex dd, 3 mixed (complex-double factors of a complex-dd system:
+// the double matrix planes plus the dd solution, four partial residuals and the corrections)
 size_t newton_matrix_bytes(int prec, int n) {
-    const int W = prec == 1 ? 2 : 4;
-    return (size_t(W) * n * (n + 1) + 2 * size_t(W) * n) * sizeof(double);
+    const int W = prec == 2 ? 4 : 2;
+    const size_t extra = prec == 3 ? (4 + 16 + 2) * size_t(n) : 0;
+    return (size_t(W) * n * (n + 1) + 2 * size_t(W) * n + extra) * sizeof(double);
 }
 size_t newton_int_bytes(int n) { return size_t(newton_int_words(n)) * sizeof(double); }
 

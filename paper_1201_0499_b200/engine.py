@@ -408,6 +408,14 @@ def _flags(precision: str, order: str | None) -> int:
     raise ValueError(f"unknown precision {precision!r} (expected 'd' or 'dd')")
 
 
+def _nflags(precision: str, order: str | None) -> int:
+    """Newton solves: 'd', 'dd', or 'mixed' (complex dd in and out, the Jacobian factored in complex
+    double and refined with complex-dd residuals: PJ_NEWTON_MIXED, n <= 32)."""
+    if precision == "mixed":
+        return _flags("dd", order) | _lib.PJ_NEWTON_MIXED
+    return _flags(precision, order)
+
+
 class EvaluationContext:
     """Owns the packed system on one GPU (uploaded once) and evaluates points there.
 
@@ -637,7 +645,9 @@ class EvaluationContext:
         """`iters` Newton steps x <- x + J(x)^-1 (y - f(x)) per point, on the GPU.
         points (and target y, optional; absent = the roots of f): [B, n, W] float64.
         Returns (points_out [B, n, W], norms [B, 2] = max-norms of y - f and of the last step,
-        status [B] int32: 0 ok, 1 singular Jacobian, 2 non-finite result). out / norms / status may be
+        status [B] int32: 0 ok, 1 singular Jacobian, 2 non-finite result, 3 mixed solve not converged).
+        precision: 'd', 'dd' or 'mixed' (dd points; the Jacobian factored in complex double and refined
+        with dd residuals — faster, for Jacobians that are not ill-conditioned). out / norms / status may be
         preallocated (page-locked buffers give full H2D / compute / D2H overlap)."""
         W = 2 if precision == "d" else 4
         pts = np.ascontiguousarray(points, np.float64)
@@ -658,7 +668,7 @@ class EvaluationContext:
         for a, shp, dt in ((out, pts.shape, np.float64), (norms, (B, 2), np.float64), (status, (B,), np.int32)):
             if a.shape != shp or a.dtype != dt or not a.flags.c_contiguous:
                 raise ValueError("newton: output buffer must be C-contiguous %s of shape %s" % (np.dtype(dt), shp))
-        check(lib().pj_newton_host(self._h, _flags(precision, order), pts.ctypes.data,
+        check(lib().pj_newton_host(self._h, _nflags(precision, order), pts.ctypes.data,
                                    tg.ctypes.data if tg is not None else None, B, iters, out.ctypes.data,
                                    norms.ctypes.data, status.ctypes.data))
         self._add_tally(B * iters)
@@ -684,7 +694,7 @@ class EvaluationContext:
         pt = self._dev_tensor(what + ": target", target, (B, n, W)) if target is not None else None
         pn = self._dev_tensor(what + ": norms", norms, (B, 2)) if norms is not None else None
         ps = self._dev_tensor(what + ": status", status, (B,), "int32") if status is not None else None
-        check(lib().pj_newton_solve(self._h, _flags(precision, None), pe, pp, pt, B, po, pn, ps,
+        check(lib().pj_newton_solve(self._h, _nflags(precision, None), pe, pp, pt, B, po, pn, ps,
                                     ctypes.c_void_p(self._stream(stream, points))))
 
     def newton_step_device(self, points, work, out, precision: str = "dd", target=None, norms=None, status=None,
@@ -700,7 +710,7 @@ class EvaluationContext:
         pt = self._dev_tensor(what + ": target", target, (B, n, W)) if target is not None else None
         pn = self._dev_tensor(what + ": norms", norms, (B, 2)) if norms is not None else None
         ps = self._dev_tensor(what + ": status", status, (B,), "int32") if status is not None else None
-        check(lib().pj_newton_step(self._h, _flags(precision, order), pp, pt, B, pw, po, pn, ps,
+        check(lib().pj_newton_step(self._h, _nflags(precision, order), pp, pt, B, pw, po, pn, ps,
                                    ctypes.c_void_p(self._stream(stream, points))))
 
     # ---- index maps (bit-exact with the reference)
@@ -721,7 +731,7 @@ class EvaluationContext:
     def set_launch(self, precision: str, threads: int = 0, tile_points: int = 0, order: str | None = None,
                    newton: bool = False) -> None:
         """Override the launch shape of the evaluation kernel (or, newton=True, the Newton solve)."""
-        f = _flags(precision, order) | (_lib.PJ_OP_NEWTON if newton else 0)
+        f = (_nflags(precision, order) | _lib.PJ_OP_NEWTON) if newton else _flags(precision, order)
         check(lib().pj_set_launch(self._h, f, threads, tile_points))
 
     def set_variant(self, variant: int, precision: str = "dd", newton: bool = False) -> None:
@@ -735,7 +745,7 @@ class EvaluationContext:
     def launch(self, precision: str, order: str | None = None, newton: bool = False):
         t, tp, b, var = ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32(), ctypes.c_int32()
         sm = ctypes.c_int64()
-        f = _flags(precision, order) | (_lib.PJ_OP_NEWTON if newton else 0)
+        f = (_nflags(precision, order) | _lib.PJ_OP_NEWTON) if newton else _flags(precision, order)
         check(lib().pj_get_launch(self._h, f, ctypes.byref(t), ctypes.byref(tp),
                                   ctypes.byref(b), ctypes.byref(sm), ctypes.byref(var)))
         return dict(threads=t.value, tile_points=tp.value, blocks=b.value, smem_bytes=sm.value, variant=var.value)

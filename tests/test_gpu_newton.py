@@ -205,3 +205,85 @@ def test_panel_kernel_bit_identical(prec, gpu):
         assert np.array_equal(got[0].view(np.uint64), want[0].view(np.uint64))
     with pytest.raises(ValueError):
         pj.EvaluationContext(pj.random_system(40, 4, 3, 2, 1)).set_variant(1, "dd", newton=True)
+
+
+# ---- the mixed-precision solve (PJ_NEWTON_MIXED): complex-double factors + dd refinement
+MIXED_SHAPES = [(32, 32, 8, 2, 64), (8, 3, 3, 5, 33), (1, 1, 1, 1, 5), (20, 10, 16, 10, 6), (31, 17, 4, 3, 40)]
+
+
+@pytest.mark.parametrize("shape", MIXED_SHAPES, ids=lambda s: "n%d_m%d_k%d_d%d_B%d" % s)
+@pytest.mark.parametrize("with_target", [False, True])
+def test_mixed_solver_bit_exact_vs_oracle(shape, with_target, gpu):
+    n, m, k, d, B = shape
+    s, S, pts = shaped(n, m, k, d, B)
+    ctx = pj.EvaluationContext(s)
+    p = pj.to_dd(pts)
+    p[..., 1] = p[..., 0] * 2.0 ** -56
+    ev = O.evaluate("dd", S, p)
+    tg = 0.5 * np.roll(ev[:, :n], 1, axis=0) if with_target else None
+    want = O.newton_solve("mixed", n, ev, p, target=tg)
+    got = solve_gpu(ctx, "mixed", ev, p, target=tg)
+    assert np.array_equal(got[2], want[2])
+    assert np.array_equal(got[0].view(np.uint64), want[0].view(np.uint64))
+    assert np.array_equal(got[1].view(np.uint64), want[1].view(np.uint64))
+
+
+@pytest.mark.parametrize("path", [p for p in NEWTON_GOLDEN if int(np.load(p)["n"]) <= 32],
+                         ids=lambda p: p.split("/")[-1])
+def test_mixed_solver_vs_mpmath(path, gpu):
+    z = np.load(path)
+    n = int(z["n"])
+    s = pj.PolynomialSystem(n, int(z["m"]), int(z["k"]), int(z["d"]), z["pos"].reshape(-1, int(z["k"])),
+                            z["exps"].reshape(-1, int(z["k"])), z["coeffs"])
+    ctx = pj.EvaluationContext(s)
+    ev = z["evals_dd"]
+    B = ev.shape[0]
+    dx, norms, status = solve_gpu(ctx, "mixed", ev, np.zeros((B, n, 4)))
+    assert np.all(status == 0)
+    assert np.all(fwd_err(dx, z["dx_dd"], "dd") <= 1e-29)
+
+
+def test_mixed_step_and_host_bit_exact_vs_oracle(gpu):
+    import torch
+    s, S, pts = shaped(32, 32, 8, 2, 3000)
+    ctx = pj.EvaluationContext(s)
+    p = pj.to_dd(pts)
+    # host path, 2 iterations, dd reference order evaluation (bit-exact with the oracle's)
+    got, gn, gs = ctx.newton_host(p[:300], "mixed", iters=2, order="ref")
+    x = p[:300]
+    for _ in range(2):
+        x, wn, ws = O.newton_solve("mixed", 32, O.evaluate("dd", S, x), x)
+    assert np.array_equal(gs, ws)
+    assert np.array_equal(got.view(np.uint64), x.view(np.uint64))
+    # device step (chunked over two streams for a large batch) = solve on the evaluator's output
+    xd = torch_dev(p)
+    work = torch.empty((3000, 32 + 1024, 4), dtype=torch.float64, device="cuda")
+    out = torch.empty_like(xd)
+    st = torch.empty(3000, dtype=torch.int32, device="cuda")
+    ctx.newton_step_device(xd, work, out, "mixed", status=st, order="ref")
+    torch.cuda.synchronize()
+    want = O.newton_solve("mixed", 32, O.evaluate("dd", S, p), p)
+    assert np.array_equal(st.cpu().numpy(), want[2])
+    assert np.array_equal(out.cpu().numpy().view(np.uint64), want[0].view(np.uint64))
+
+
+def test_mixed_rejects_large_n_and_flags_ill_conditioning(gpu):
+    s, S, pts = shaped(33, 31, 7, 3, 2)
+    ctx = pj.EvaluationContext(s)
+    p = pj.to_dd(pts)
+    ev = O.evaluate("dd", S, p)
+    with pytest.raises(ValueError, match="n <= 32"):
+        solve_gpu(ctx, "mixed", ev, p)
+    s, S, pts = shaped(32, 32, 8, 2, 1)
+    ctx = pj.EvaluationContext(s)
+    p = pj.to_dd(pts)
+    ev = O.evaluate("dd", S, p)
+    J = ev[0, 32:].reshape(32, 32, 4)
+    J[1] = J[0]
+    J[1, :, 0] *= 1.0 + 2.0 ** -40
+    J[1, :, 1] = 0.0
+    J[1, :, 3] = 0.0
+    got = solve_gpu(ctx, "mixed", ev, p)
+    want = O.newton_solve("mixed", 32, ev, p)
+    assert got[2][0] == 3 == want[2][0]
+    assert np.array_equal(got[0].view(np.uint64), want[0].view(np.uint64))

@@ -139,3 +139,57 @@ def test_oracle_newton_quadratic_convergence_to_target():
         errs.append(float(np.max(np.abs((x[..., 0] - xs[..., 0]) + (x[..., 1] - xs[..., 1])))))
     assert errs[2] < 1e-10 and errs[3] < 1e-20
     assert errs[-1] < 1e-29, errs
+
+
+# ---- the mixed-precision solve (PJ_NEWTON_MIXED): complex-double factors + dd refinement
+@pytest.mark.parametrize("path", [p for p in NEWTON_GOLDEN if int(np.load(p)["n"]) <= 32],
+                         ids=lambda p: p.split("/")[-1])
+def test_oracle_newton_mixed_matches_mpmath(path):
+    """Two refinement steps with complex-dd residuals reach the dd solve's accuracy on the
+    mpmath-pinned cases (well-conditioned: the factors only need cond(J) * 2^-52 << 1)."""
+    z = np.load(path)
+    n = int(z["n"])
+    ev = z["evals_dd"]
+    B = ev.shape[0]
+    dx, norms, status = O.newton_solve("mixed", n, ev, np.zeros((B, n, 4)))
+    assert np.all(status == 0), status
+    err = fwd_err(dx, z["dx_dd"], "dd")
+    assert np.all(err <= np.maximum(n * z["cond"] * U["dd"], 1e-29)), err
+    assert np.all(err <= 1e-29)
+
+
+def test_oracle_newton_mixed_vs_dd_solve_and_status():
+    s, S = c1()
+    pts = pj.to_dd(pj.random_points(32, 8, 11))
+    ev = O.evaluate("dd", S, pts)
+    xm, nm, stm = O.newton_solve("mixed", 32, ev, pts)
+    xd, nd, std = O.newton_solve("dd", 32, ev, pts)
+    assert np.all(stm == 0) and np.all(std == 0)
+    assert np.array_equal(nm[:, 0], nd[:, 0])  # same residual norm (the dd rhs)
+    # both solves agree to dd accuracy relative to the step
+    err = fwd_err(xm - pts, xd - pts, "dd")
+    assert np.all(err <= 1e-28), err
+    # an ill-conditioned Jacobian (rows nearly dependent at 2^-40) is flagged: status 3, not a
+    # silently inaccurate step
+    ev2 = ev[:1].copy()
+    J = ev2[0, 32:].reshape(32, 32, 4)
+    J[1] = J[0]
+    J[1, :, 0] *= 1.0 + 2.0 ** -40
+    J[1, :, 1] = 0.0
+    J[1, :, 3] = 0.0
+    _, _, st2 = O.newton_solve("mixed", 32, ev2, pts[:1])
+    _, _, st2d = O.newton_solve("dd", 32, ev2, pts[:1])
+    assert st2d[0] == 0 and st2[0] == 3, (st2, st2d)
+
+
+def test_oracle_newton_mixed_singular_and_size_limit():
+    s = permutation_system(12)
+    S = sysd_of(s)
+    pts = pj.to_dd(pj.random_points(12, 2, 5))
+    ev = O.evaluate("dd", S, pts)
+    ev[0, 12:] = 0.0  # zero Jacobian: singular
+    xo, norms, status = O.newton_solve("mixed", 12, ev, pts)
+    assert status[0] == 1 and np.isinf(norms[0, 1]) and np.array_equal(xo[0], pts[0])
+    assert status[1] == 0
+    with pytest.raises(RuntimeError):
+        O.newton_solve("mixed", 40, np.zeros((1, 40 + 1600, 4)), np.zeros((1, 40, 4)))

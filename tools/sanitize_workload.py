@@ -36,6 +36,8 @@ for (n, m, k, d), wide, B in cases:
     if n <= 256:
         ctx.newton_host(pts(n, B, 11, "dd"), "dd", iters=2)
         ctx.newton_host(pts(n, B, 11, "d"), "d", iters=1)
+    if n <= 32:
+        ctx.newton_host(pts(n, B, 11, "dd"), "mixed", iters=2)
     print(f"ok n={n} m={m} k={k} d={d}", flush=True)
 # Newton with a global slab (n > 64 dd) and the pipelined host path with several chunks
 s = pj.random_system(100, 7, 5, 4, 7)
