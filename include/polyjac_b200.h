@@ -221,7 +221,7 @@ int64_t pj_system_write_text(const pj_system_desc* sys, char* buf, int64_t cap);
  *   points_out  [batch][n][W]; may alias points (in-place update)
  *   norms       [batch][2] or NULL: max over i of max(|Re hi|, |Im hi|) of (y - f)_i, of dx_i
  *   status      [batch] or NULL: 0 ok, 1 singular (a zero pivot column; x_new = x, norms[1] = inf),
- *               2 non-finite result
+ *               2 non-finite result, 3 (PJ_NEWTON_MIXED only) the refinement has not converged
  * Asynchronous on `stream`; no allocation for n <= 64 (larger n allocates per-CTA matrix slabs
  * on first use). */
 int pj_newton_solve(pj_ctx* ctx, int flags, const double* d_evals, const double* d_points, const double* d_target,
