@@ -283,11 +283,13 @@ public:
 
     // Newton corrector (B200 addition): `iters` steps x <- x + J(x)^-1 (y - f(x))
     // per point on the GPU, host buffers [batch][n] (target y may be null: the roots of f).
-    // norms [batch][2] (|y - f|, |last step|) and status [batch] (0 ok, 1 singular, 2 non-finite)
-    // may be null.
+    // norms [batch][2] (|y - f|, |last step|) and status [batch] (0 ok, 1 singular, 2 non-finite,
+    // 3 mixed refinement not converged) may be null. mixed = true (n <= 32): the Jacobian factored
+    // in complex double and refined with dd residuals (PJ_NEWTON_MIXED; faster, for Jacobians that
+    // are not ill-conditioned).
     void newton_dd(const ComplexDD* points, const ComplexDD* target, std::int64_t batch, int iters, ComplexDD* out,
-                   double* norms = nullptr, std::int32_t* status = nullptr) {
-        detail::check(pj_newton_host(ctx_, PJ_PREC_DD, reinterpret_cast<const double*>(points),
+                   double* norms = nullptr, std::int32_t* status = nullptr, bool mixed = false) {
+        detail::check(pj_newton_host(ctx_, PJ_PREC_DD | (mixed ? PJ_NEWTON_MIXED : 0), reinterpret_cast<const double*>(points),
                                      reinterpret_cast<const double*>(target), batch, iters,
                                      reinterpret_cast<double*>(out), norms, status));
         tally(batch * iters);

@@ -157,6 +157,11 @@ int main() {
         ctx.newton_dd(x, nullptr, 1, 1, xo, norms, &st);
         CHECK(st == 0 && norms[0] == 0.9);
         for (const auto& v : xo) CHECK(v.re_hi == 0 && v.re_lo == 0 && v.im_hi == 0 && v.im_lo == 0);
+        // the mixed-precision solve: double factors + dd refinement reach the same exact root
+        st = -1;
+        ctx.newton_dd(x, nullptr, 1, 1, xo, norms, &st, /*mixed=*/true);
+        CHECK(st == 0 && norms[0] == 0.9);
+        for (const auto& v : xo) CHECK(v.re_hi == 0 && v.re_lo == 0 && v.im_hi == 0 && v.im_lo == 0);
         PolynomialSystem sing{2, 1, 1, 1, {}};
         sing.terms = {{{1.0, 0.0}, {{0}, {1}}}, {{2.0, 0.0}, {{0}, {1}}}};
         polyjac_b200::dropin::EvaluationContext c2(sing);
