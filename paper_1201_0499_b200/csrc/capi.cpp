@@ -445,6 +445,16 @@ struct pj_ctx {
     static constexpr size_t kSmallOut = size_t(1) << 20;
     char* h_small = nullptr;
     size_t h_small_in = 0;  // bytes of the points part (results follow, then one int)
+    // ... replayed as one CUDA graph (flag reset, H2D, kernel, D2H x 2, flag reset) for the last
+    // (flags, batch, buffers, launch shape) it was captured for
+    struct SmallGraph {
+        cudaGraphExec_t exec = nullptr;
+        int flags = 0;
+        int64_t batch = 0;
+        const void *d_in = nullptr, *d_out = nullptr, *h = nullptr;
+        int variant = 0, blocks = 0, threads = 0, tp = 0;
+        size_t smem = 0;
+    } sgraph;
     cudaStream_t hstream[kHostStreams] = {};
     cudaEvent_t hdone[kHostStreams] = {};
     cudaEvent_t nfork = nullptr;  // pj_newton_step fork event
@@ -549,6 +559,7 @@ void free_ctx(pj_ctx* c) {
     }
     if (c->nfork) cudaEventDestroy(c->nfork);
     if (c->h_small) cudaFreeHost(c->h_small);
+    if (c->sgraph.exec) cudaGraphExecDestroy(c->sgraph.exec);
     cudaSetDevice(prev);
     delete c;
 }
@@ -1550,16 +1561,65 @@ int pj_evaluate_host(pj_ctx* ctx, int flags, const double* h_points, int64_t bat
         int* hflag = reinterpret_cast<int*>(hout + pj_ctx::kSmallOut);
         cudaStream_t st = ctx->hstream[0];
         std::memcpy(hin, h_points, in_b);
-        PJ_CUDA(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), st));
-        PJ_CUDA(cudaMemcpyAsync(ctx->d_in[0], hin, in_b, cudaMemcpyHostToDevice, st));
-        int rc = pj_evaluate(ctx, flags, ctx->d_in[0], batch, ctx->d_out[0], st);
-        if (rc) {
-            cudaStreamSynchronize(st);
-            return rc;
+        // the six stream operations, enqueued directly or captured into the context's graph
+        auto enqueue = [&]() -> int {
+            cudaError_t e;
+            if ((e = cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), st)) ||
+                (e = cudaMemcpyAsync(ctx->d_in[0], hin, in_b, cudaMemcpyHostToDevice, st)))
+                return cuda_fail(e, "evaluate_host");
+            if (int rc = pj_evaluate(ctx, flags, ctx->d_in[0], batch, ctx->d_out[0], st)) return rc;
+            if ((e = cudaMemcpyAsync(hout, ctx->d_out[0], out_b, cudaMemcpyDeviceToHost, st)) ||
+                (e = cudaMemcpyAsync(hflag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st)) ||
+                (e = cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), st)))
+                return cuda_fail(e, "evaluate_host");
+            return PJ_OK;
+        };
+        // graph replay (one launch instead of six operations), not for PJ_VALIDATE (its check reads
+        // the verdict back inside pj_evaluate); any capture failure falls back to direct enqueueing
+        bool replay = !(flags & PJ_VALIDATE);
+        if (replay) {
+            pj_ctx::SmallGraph& G = ctx->sgraph;
+            const pjb::LaunchCfg& Lc = ctx->mode[mode_of(flags)].cfg;
+            const bool match = G.exec && G.flags == flags && G.batch == batch && G.d_in == ctx->d_in[0] &&
+                               G.d_out == ctx->d_out[0] && G.h == ctx->h_small && G.variant == Lc.variant &&
+                               G.blocks == Lc.blocks && G.threads == Lc.threads && G.tp == Lc.tp &&
+                               G.smem == Lc.smem_bytes;
+            if (!match) {
+                if (G.exec) cudaGraphExecDestroy(G.exec);
+                G.exec = nullptr;
+                cudaGraph_t g = nullptr;
+                bool ok = cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal) == cudaSuccess;
+                if (ok) {
+                    const int rc = enqueue();
+                    ok = cudaStreamEndCapture(st, &g) == cudaSuccess && rc == PJ_OK && g;
+                    ok = ok && cudaGraphInstantiate(&G.exec, g, 0) == cudaSuccess;
+                    if (g) cudaGraphDestroy(g);
+                }
+                if (ok) {
+                    G.flags = flags;
+                    G.batch = batch;
+                    G.d_in = ctx->d_in[0];
+                    G.d_out = ctx->d_out[0];
+                    G.h = ctx->h_small;
+                    G.variant = Lc.variant;
+                    G.blocks = Lc.blocks;
+                    G.threads = Lc.threads;
+                    G.tp = Lc.tp;
+                    G.smem = Lc.smem_bytes;
+                } else {
+                    G.exec = nullptr;
+                    cudaGetLastError();  // a failed capture leaves no sticky error behind
+                    replay = false;
+                }
+            }
+            if (replay) PJ_CUDA(cudaGraphLaunch(G.exec, st));
         }
-        PJ_CUDA(cudaMemcpyAsync(hout, ctx->d_out[0], out_b, cudaMemcpyDeviceToHost, st));
-        PJ_CUDA(cudaMemcpyAsync(hflag, ctx->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-        PJ_CUDA(cudaMemsetAsync(ctx->d_flag, 0, sizeof(int), st));
+        if (!replay) {
+            if (int rc = enqueue()) {
+                cudaStreamSynchronize(st);
+                return rc;
+            }
+        }
         PJ_CUDA(cudaStreamSynchronize(st));
         if (*hflag) return fail(PJ_ENONFINITE, "evaluate: non-finite coordinate");
         std::memcpy(h_out, hout, out_b);
