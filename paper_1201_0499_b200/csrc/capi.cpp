@@ -1576,7 +1576,8 @@ int pj_evaluate_host(pj_ctx* ctx, int flags, const double* h_points, int64_t bat
         };
         // graph replay (one launch instead of six operations), not for PJ_VALIDATE (its check reads
         // the verdict back inside pj_evaluate); any capture failure falls back to direct enqueueing
-        bool replay = !(flags & PJ_VALIDATE);
+        // (nor for global-scratch launches: the slab pointer is re-read at every launch and may move)
+        bool replay = !(flags & PJ_VALIDATE) && !ctx->mode[mode_of(flags)].cfg.gscratch;
         if (replay) {
             pj_ctx::SmallGraph& G = ctx->sgraph;
             const pjb::LaunchCfg& Lc = ctx->mode[mode_of(flags)].cfg;
