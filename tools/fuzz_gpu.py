@@ -65,4 +65,42 @@ for c in range(cases):
         assert np.array_equal(st.cpu().numpy(), ws), (prec, n, m, k, d, seed)
         assert np.array_equal(out.cpu().numpy().view(np.uint64), wx.view(np.uint64)), ("newton " + prec, n, m, k, d, seed)
     print(f"case {c}: n={n} m={m} k={k} d={d} B={B} ok (dd fast {e:.2e})", flush=True)
-print(f"all {cases} cases ok; worst dd fast error {worst:.3e} x sum|terms|")
+# ragged systems (per-polynomial m, per-term k): complex double and dd reference order bit-exact
+# with the ragged restatement, dd fast order within the tolerance
+for c in range(cases // 2):
+    n = int(rng.integers(1, 40))
+    d = int(rng.choice([1, 2, 3, 6]))
+    mlo = int(rng.integers(1, 20)); mhi = mlo + int(rng.integers(0, 40))
+    klo = int(rng.integers(1, min(n, 10) + 1)); khi = min(n, klo + int(rng.integers(0, 8)))
+    B = int(rng.choice([1, 5, 64, 300]))
+    seed = int(rng.integers(1, 1 << 30))
+    r = pj.random_ragged_system(n, (mlo, mhi), (klo, khi), d, seed)
+    ctx = pj.EvaluationContext(r)
+    R = r.as_dict()
+    pts = pj.random_points(n, B, seed + 3)
+    p2 = np.stack([pts.real, pts.imag], -1)
+    p4 = pj.to_dd(pts)
+    got = ctx.evaluate_host(p2, "d")
+    want = O.evaluate_ragged("d", R, p2)
+    assert np.array_equal(got.view(np.uint64), want.view(np.uint64)), ("ragged d", n, d, mlo, mhi, klo, khi, seed)
+    want4, ms = O.evaluate_ragged("dd", R, p4, magsum=True)
+    assert np.array_equal(ctx.evaluate_dd(p4, order="ref").view(np.uint64), want4.view(np.uint64)), ("ragged dd ref", seed)
+    e = dd_rel(ctx.evaluate_dd(p4), want4, ms)
+    assert e <= 1e-30, ("ragged dd fast", seed, e)
+    print(f"ragged {c}: n={n} d={d} m=[{mlo},{mhi}] k=[{klo},{khi}] B={B} ok", flush=True)
+# the wide encoding (n > 256)
+for c in range(4):
+    n = int(rng.integers(257, 700))
+    s = pj.random_system(n, int(rng.integers(1, 4)), int(rng.integers(1, 6)), int(rng.choice([2, 4])), 11 + c)
+    ctx = pj.EvaluationContext(s, wide=True)
+    S = sysd(s)
+    pts = pj.random_points(n, 2, 5 + c)
+    p2 = np.stack([pts.real, pts.imag], -1)
+    got = ctx.evaluate_host(p2, "d")
+    assert np.array_equal(got.view(np.uint64), O.evaluate("d", S, p2).view(np.uint64)), ("wide d", n)
+    p4 = pj.to_dd(pts)
+    want4, ms = O.evaluate("dd", S, p4, magsum=True)
+    assert np.array_equal(ctx.evaluate_dd(p4, order="ref").view(np.uint64), want4.view(np.uint64)), ("wide ref", n)
+    assert dd_rel(ctx.evaluate_dd(p4), want4, ms) <= 1e-30, ("wide fast", n)
+    print(f"wide {c}: n={n} ok", flush=True)
+print(f"all {cases} uniform, {cases // 2} ragged and 4 wide cases ok; worst uniform dd fast error {worst:.3e} x sum|terms|")
