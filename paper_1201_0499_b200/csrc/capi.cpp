@@ -1437,16 +1437,15 @@ int pj_evaluate(pj_ctx* ctx, int flags, const double* d_points, int64_t batch, d
             return fail(PJ_ENONFINITE, "evaluate: non-finite coordinate");
         }
     }
-    if (L.variant == 1) {
+    if (L.variant == 1 || L.variant == 2) {
         // a batch with fewer tiles than CTAs (C1: one point) spreads each tile's tasks over
         // several CTAs, one task per warp at most, instead of leaving all but a few SMs idle; the
-        // grid shrinks to the CTAs that have work (a multiple of the split, eval_fast.cu). (The
-        // complex-double kernel keeps one CTA per tile: its 128-register budget has no room for
-        // the split's loop state.)
+        // grid shrinks to the CTAs that have work (a multiple of the split, eval_fast.cu; the
+        // complex-double kernel runs a separate split instantiation, eval_fastd.cu)
         const long long ntiles = (batch + L.tp - 1) / L.tp;
         if (ntiles < L.blocks) {
             const long long in_tile = std::min<long long>(batch, L.tp);
-            const long long tasks = in_tile * ctx->n;
+            const long long tasks = (L.variant == 2 ? (in_tile + 1) / 2 : in_tile) * ctx->n;
             const long long nw = L.threads / 32;
             L.splits = int(std::max(1LL, std::min<long long>(L.blocks / ntiles, (tasks + nw - 1) / nw)));
             L.blocks = int(std::min<long long>(L.blocks, ntiles * L.splits));

@@ -57,10 +57,13 @@ constexpr int kVPer = PJB_FASTD_VPER;  // value-chain terms per stage-3 loop ite
 template <int K>
 constexpr int fastd_min_blocks() { return PJB_FASTD_MINB(K); }
 
-template <int K, bool D2>
+// SPLIT: the small-batch instantiation (a batch with fewer tiles than CTAs): SP CTAs share each
+// tile's tasks (see eval_fast.cu). A separate instantiation, so the split's loop state never
+// touches the register budget of the main kernel (128 registers, no room)
+template <int K, bool D2, bool SPLIT = false>
 __global__ void __launch_bounds__(256, fastd_min_blocks<K>()) fastd_kernel(DevSystem S, const double* __restrict__ pts,
                                                     double* __restrict__ out, long long B, int TP,
-                                                    int* __restrict__ flag) {
+                                                    int* __restrict__ flag, int SP) {
     constexpr int W = 2;
     // staging: slot (j, point u) of lane g at ((j * kP + u) * 32 + g) * W (re, im adjacent)
     constexpr int stgW = (K + 1) * kP * W * 32;
@@ -78,7 +81,7 @@ __global__ void __launch_bounds__(256, fastd_min_blocks<K>()) fastd_kernel(DevSy
     const CD one = {1.0, 0.0};
     const CD zero = {0.0, 0.0};
 
-    for (long long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    for (long long tile = SPLIT ? blockIdx.x / SP : blockIdx.x; tile < ntiles; tile += SPLIT ? gridDim.x / SP : gridDim.x) {
         const long long b0 = tile * TP;
         const int tp = (int)min((long long)TP, B - b0);
         for (int i = threadIdx.x; i < tp * n; i += blockDim.x) {
@@ -102,7 +105,7 @@ __global__ void __launch_bounds__(256, fastd_min_blocks<K>()) fastd_kernel(DevSy
             __syncthreads();
         }
         const int npairs = (tp + 1) / 2;
-        for (int task = warp; task < npairs * n; task += nw) {
+        for (int task = SPLIT ? warp + (int)(blockIdx.x % SP) * nw : warp; task < npairs * n; task += SPLIT ? nw * SP : nw) {
             const int p = task / npairs, pair = task - p * npairs;
             const int t0 = 2 * pair;
             const bool has1 = t0 + 1 < tp;
@@ -326,12 +329,12 @@ namespace {
 template <int K, bool D2>
 cudaError_t launch_dt(const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,
                       cudaStream_t st) {
-    auto kern = fastd_kernel<K, D2>;
+    auto kern = L.splits > 1 ? fastd_kernel<K, D2, true> : fastd_kernel<K, D2, false>;
     if (L.smem_bytes > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dyn_smem_limit((const void*)kern));
         if (e != cudaSuccess) return e;
     }
-    kern<<<L.blocks, L.threads, L.smem_bytes, st>>>(S, pts, out, B, L.tp, L.flag);
+    kern<<<L.blocks, L.threads, L.smem_bytes, st>>>(S, pts, out, B, L.tp, L.flag, L.splits);
     return cudaGetLastError();
 }
 template <int K, bool D2>

@@ -71,7 +71,7 @@ struct LaunchCfg {
     double* gscratch = nullptr;  // non-null: tables/staging in global memory (huge systems)
     int* flag = nullptr;      // device int, set to 1 on a non-finite coordinate
     int producers = 0;        // warp-specialised dd kernel (variant 3): producer warps per CTA
-    int splits = 1;           // fast dd kernel (variant 1): CTAs sharing one tile's tasks — set per
+    int splits = 1;           // fast kernels (variants 1, 2): CTAs sharing one tile's tasks — set per
                               // launch for batches with fewer tiles than CTAs (pj_evaluate)
 };
 
