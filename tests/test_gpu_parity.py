@@ -445,3 +445,10 @@ def test_small_batches_split_tiles_bit_identical(shape, gpu):
     assert np.array_equal(got1.view(np.uint64), full[B - 1:].view(np.uint64))
     want, ms = O.evaluate("dd", S, p4[:7], magsum=True)
     assert dd_rel(full[:7], want, ms) <= DD_TOL
+    # complex double (its split runs a separate kernel instantiation): bit-exact with the
+    # reference at every batch size
+    p2 = np.ascontiguousarray(p4[..., [0, 2]])
+    full_d = ctx.evaluate_host(p2, "d")
+    for b in [1, 2, 3, 7, 100]:
+        assert np.array_equal(ctx.evaluate_host(p2[:b], "d").view(np.uint64), full_d[:b].view(np.uint64)), b
+    assert np.array_equal(full_d[:3].view(np.uint64), ref_double(S, p2[:3]).view(np.uint64))
