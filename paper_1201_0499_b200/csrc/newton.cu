@@ -603,11 +603,14 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, nt_min_blocks<T, NQ, MX
         __syncthreads();
         PJB_PH(0)
 #if PJB_NT_PREFETCH
-        // pull the CTA's next point into L2 while this one is eliminated: its load then waits on L2
-        // instead of DRAM (measured: the load phase took ~25k cycles per point under full load)
-        if (b + gridDim.x < a.B) {
-            const char* nx = reinterpret_cast<const char*>(a.evals + size_t(b + gridDim.x) * (size_t(n) * n + n) * W);
-            const int lines = int((size_t(n) * n + n) * W * sizeof(double) / 128);
+        // complex-double factorisations (the d solve and the mixed solve) pull the CTA's next point
+        // into L2 while this one is eliminated (measured: d 2.21 -> 2.18 ms; the dd solve, 0.5%
+        // slower with it, does not; the mixed solve 4.23 -> 4.20 ms with the right element width:
+        // profiles/r02_newton_l2prefetch_ab.log, r02_newton_prefetch_w.log, r02_newton_prefetch_w_ab.log)
+        if (W == 2 && b + gridDim.x < a.B) {
+            constexpr int WE = MX ? 4 : W;  // the evaluator output's element width
+            const char* nx = reinterpret_cast<const char*>(a.evals + size_t(b + gridDim.x) * (size_t(n) * n + n) * WE);
+            const int lines = int((size_t(n) * n + n) * WE * sizeof(double) / 128);
             for (int l = tid; l < lines; l += nt) asm volatile("prefetch.global.L2 [%0];" ::"l"(nx + size_t(l) * 128));
         }
 #endif
