@@ -151,3 +151,27 @@ def test_newton_chunked_paths_on_global_slabs_match_one_launch(torch_cuda):
     ctx.newton_step_device(xd, work, xo2, "dd")
     torch.cuda.synchronize()
     assert torch.equal(xo2, xo)
+
+
+def test_small_host_batches_graph_replay_semantics(torch_cuda):
+    # small host batches replay one cached CUDA graph (csrc/capi.cpp, pj_evaluate_host): a
+    # non-finite point is still rejected, the flag does not leak into the next call, and changes
+    # of batch size or precision (re-capture) keep the results identical to a fresh context's
+    s = pj.random_system(12, 9, 4, 2, 21)
+    ctx, fresh = pj.EvaluationContext(s), pj.EvaluationContext(s)
+    pts = pj.to_dd(pj.random_points(12, 5, 22))
+    bad = pts.copy()
+    bad[2, 7, 0] = float("nan")
+    first = ctx.evaluate_dd(pts)
+    with pytest.raises(ValueError, match="non-finite"):
+        ctx.evaluate_dd(bad)
+    for _ in range(3):  # replays after the failed call: no stale flag, same bits
+        assert np.array_equal(ctx.evaluate_dd(pts).view(np.uint64), first.view(np.uint64))
+    p2 = np.ascontiguousarray(pts[..., [0, 2]])
+    for b in [1, 5, 2, 5, 1]:  # alternate batch sizes and precisions
+        assert np.array_equal(ctx.evaluate_dd(pts[:b]).view(np.uint64), fresh.evaluate_dd(pts[:b]).view(np.uint64))
+        assert np.array_equal(ctx.evaluate_host(p2[:b], "d").view(np.uint64),
+                              fresh.evaluate_host(p2[:b], "d").view(np.uint64))
+    # a launch-shape change invalidates the cached graph
+    ctx.set_launch("dd", 128, 1)
+    assert np.array_equal(ctx.evaluate_dd(pts).view(np.uint64), first.view(np.uint64))
