@@ -373,7 +373,7 @@ void evaluate_range(const System& S, const double* pts, long b0, long b1, double
 // Restates the operation order defined in paper_1201_0499_b200/csrc/newton.cu (the reference
 // has no Newton step): rhs = y + (-f); Gaussian elimination with implicit partial
 // pivoting on |Re hi| + |Im hi| (maximum over the rows not yet pivoted, strictly positive, ties
-// to the smallest row index); pivot inverse conj(a)/|a|^2; multipliers l = A[i][kk] * inv
+// to the smallest row index); pivot inverse conj(a)/|a|^2 (dd: NT_DD::abs2, NT_DD::inv); multipliers l = A[i][kk] * inv
 // (normalised product); trailing update A[i][j] + (-(l * A[piv][j])) with the dd product left
 // unnormalised; back substitution dx_s = rhs[piv_s] * inv_s, then rhs[piv_t] + (-(A[piv_t][s] * dx_s))
 // for t < s (descending s); x + dx.
@@ -442,9 +442,17 @@ struct NT_DD {
         return std::isfinite(a.rh) && std::isfinite(a.rl) && std::isfinite(a.ih) && std::isfinite(a.il);
     }
     static CDD umul(CDD a, CDD b) { return cdd_mul_u(a, b); }
+    static DD abs2(DD re, DD im) {  // |a|^2: ordered Fast2Sum of the squares, errors in the low word
+        const double p1 = re.hi * re.hi, p2 = im.hi * im.hi;
+        double e1 = std::fma(re.hi, re.hi, -p1), e2 = std::fma(im.hi, im.hi, -p2);
+        e1 = std::fma(re.hi + re.hi, re.lo, e1);
+        e2 = std::fma(im.hi + im.hi, im.lo, e2);
+        const DD s = fast_two_sum(std::fmax(p1, p2), std::fmin(p1, p2));
+        return fast_two_sum(s.hi, s.lo + (e1 + e2));
+    }
     static CDD inv(CDD a) {
         DD re{a.rh, a.rl}, im{a.ih, a.il};
-        DD den = dd_add(dd_mul(re, re), dd_mul(im, im));
+        DD den = abs2(re, im);
         DD r = dd_rcp(den);
         DD o = dd_mul(re, r), p = dd_mul({-a.ih, -a.il}, r);
         return {o.hi, o.lo, p.hi, p.lo};

@@ -86,9 +86,20 @@ __device__ __forceinline__ CD nt_inv(CD a) {
     double r = __drcp_rn(den);
     return {__dmul_rn(a.re, r), __dmul_rn(-a.im, r)};
 }
+// |a|^2 in dd with a short dependency chain: the two squares are non-negative, so their high
+// parts are summed with an exact Fast2Sum after ordering them by size (no TwoSum), and the square
+// errors (x_hi^2 - p exactly, plus 2 x_hi x_lo) join the low word before one closing Fast2Sum
+__device__ __forceinline__ DD nt_abs2(DD re, DD im) {
+    const double p1 = __dmul_rn(re.hi, re.hi), p2 = __dmul_rn(im.hi, im.hi);
+    double e1 = __fma_rn(re.hi, re.hi, -p1), e2 = __fma_rn(im.hi, im.hi, -p2);
+    e1 = __fma_rn(__dadd_rn(re.hi, re.hi), re.lo, e1);
+    e2 = __fma_rn(__dadd_rn(im.hi, im.hi), im.lo, e2);
+    const DD s = fast_two_sum(fmax(p1, p2), fmin(p1, p2));
+    return fast_two_sum(s.hi, __dadd_rn(s.lo, __dadd_rn(e1, e2)));
+}
 __device__ __forceinline__ CDD nt_inv(CDD a) {
     DD re{a.rh, a.rl}, im{a.ih, a.il};
-    DD den = dd_add(nt_dd_mul(re, re), nt_dd_mul(im, im));
+    DD den = nt_abs2(re, im);
     DD r = nt_dd_rcp(den);
     DD o = nt_dd_mul(re, r), p = nt_dd_mul({-a.ih, -a.il}, r);
     return {o.hi, o.lo, p.hi, p.lo};
