@@ -333,8 +333,20 @@ __device__ __forceinline__ void nt_load_mixed(const NewtonArgs& a, long long b, 
 // solution [4][n] (pair layout), PART: four dd partial residuals per row [4][4n], DXC: corrections.
 __device__ __forceinline__ void nt_mixed_finish(const NewtonArgs& a, long long b, const double* A, const double* INV,
                                                 double* DXD, double* PART, double* DXC, const int* s_piv,
-                                                const int* s_step, bool singular, int warp) {
+                                                const int* s_step, bool singular, int warp, long long* phm = nullptr) {
     const int n = a.n, ld = n + 1, P = n * ld, lane = threadIdx.x & 31;
+#ifdef PJB_NT_PHASES
+    // developer instrumentation: phm[0..3] += initial solve, residual sums, refinement solves, update
+    long long tm = clock64();
+#define PJB_PHM(i)                      \
+    {                                   \
+        const long long t_ = clock64(); \
+        phm[i] += t_ - tm;              \
+        tm = t_;                        \
+    }
+#else
+#define PJB_PHM(i)
+#endif
     const double* x = a.points + size_t(b) * n * 4;
     double* xo = a.points_out + size_t(b) * n * 4;
     const double* ev = a.evals + size_t(b) * (size_t(n) * n + n) * 4;
@@ -384,6 +396,7 @@ __device__ __forceinline__ void nt_mixed_finish(const NewtonArgs& a, long long b
             NL<CDD>::st(DXD, i, n, CDD{c.re, 0.0, c.im, 0.0});
         }
     }
+    PJB_PHM(0)
     for (int it = 0; it < kMixedIters; ++it) {
         __syncthreads();  // DXD complete
         // partial residual sums: warp g, lane = row i, columns j = g, g+4, ...
@@ -395,6 +408,7 @@ __device__ __forceinline__ void nt_mixed_finish(const NewtonArgs& a, long long b
             NL<CDD>::st(PART + warp * 4 * n, lane, n, acc);
         }
         __syncthreads();
+        PJB_PHM(1)
         if (warp == 0) {
             CD bb{0.0, 0.0};
             CDD r{0.0, 0.0, 0.0, 0.0};
@@ -427,6 +441,7 @@ __device__ __forceinline__ void nt_mixed_finish(const NewtonArgs& a, long long b
             for (int o = 16; o; o >>= 1) cm = fmax(cm, __shfl_xor_sync(0xffffffffu, cm, o));
             cmax = cm;
         }
+        PJB_PHM(2)
     }
     if (warp == 0) {
         __syncwarp();
@@ -446,6 +461,8 @@ __device__ __forceinline__ void nt_mixed_finish(const NewtonArgs& a, long long b
             if (a.status) a.status[b] = !fin ? 2 : (cmax > ldexp(dn, -64) ? 3 : 0);
         }
     }
+    PJB_PHM(3)
+#undef PJB_PHM
 }
 
 // NQ: active-row slots per lane (look-ahead) and rows per lane (back substitution), n <= 32*NQ
@@ -593,8 +610,8 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, nt_min_blocks<T, NQ, MX
     };
 #ifdef PJB_NT_PHASES
     // developer instrumentation: per-CTA cycle totals of the load, elimination and back-substitution
-    // phases over all of its points, after the B status words (status must hold B + 2 + 8 * grid)
-    long long ph[4] = {0, 0, 0, 0};
+    // phases over all of its points, after the B status words (status must hold B + 2 + 16 * grid; phases 4-7 break down the mixed refinement)
+    long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     long long tph = clock64();
 #define PJB_PH(i)                      \
     {                                  \
@@ -734,7 +751,11 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, nt_min_blocks<T, NQ, MX
 
         PJB_PH(1)
         if constexpr (MX)
-            nt_mixed_finish(a, b, A, INV, DXD, PART, DXC, s_piv, s_step, singular, warp);
+            nt_mixed_finish(a, b, A, INV, DXD, PART, DXC, s_piv, s_step, singular, warp
+#ifdef PJB_NT_PHASES
+                            , ph + 4
+#endif
+            );
         else if (warp == 0)
             nt_back_substitute<T, NQ>(a, b, A, INV, DX, s_piv, s_step, singular);
         __syncthreads();  // the next point reuses the matrix storage
@@ -745,8 +766,8 @@ __global__ void __launch_bounds__(NtBounds<NQ>::threads, nt_min_blocks<T, NQ, MX
     }
 #ifdef PJB_NT_PHASES
     if (tid == 0 && a.status) {
-        long long* o = reinterpret_cast<long long*>(a.status + ((a.B + 1) & ~1LL)) + 4 * blockIdx.x;
-        for (int i = 0; i < 4; ++i) o[i] = ph[i];
+        long long* o = reinterpret_cast<long long*>(a.status + ((a.B + 1) & ~1LL)) + 8 * blockIdx.x;
+        for (int i = 0; i < 8; ++i) o[i] = ph[i];
     }
 #endif
 #undef PJB_PH

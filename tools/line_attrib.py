@@ -1,6 +1,7 @@
 """Attribute ncu per-SASS stall samples / executed instructions to source lines.
 usage: python tools/line_attrib.py <nvdisasm -gi output> <kernel mangled name> <ncu sass csv> [file-filter]"""
 import csv
+import os
 import re
 import sys
 from collections import defaultdict
@@ -46,7 +47,7 @@ for r in rows[2:]:
     tot_s += s
 srcl = {}
 try:
-    for i, t in enumerate(open([k[0] for k in ex if filt in k[0]][0]), 1):
+    for i, t in enumerate(open(os.environ.get("PJ_SRC") or [k[0] for k in ex if filt in k[0]][0]), 1):
         srcl[i] = t.strip()
 except Exception:
     pass
