@@ -41,6 +41,7 @@ for prec in (os.environ.get("PJ_PRECS", "dd,d")).split(","):
     sub = ph[:, 4:].sum(0) / cnt
     print(f"n={n} {prec} B={B} {launch}: cycles per point per CTA: load {tot[0]:.0f}, elimination {tot[1]:.0f}, "
           f"back substitution {tot[2]:.0f}, total {tot.sum():.0f}; points per CTA {ph[:, 3].min()}..{ph[:, 3].max()}"
+          + (f"; slots 4-7 {sub.round().tolist()}" if os.environ.get("PJ_ALLSLOTS") else "")
           + (f"; refinement: initial solve {sub[0]:.0f}, residuals {sub[1]:.0f}, solves {sub[2]:.0f}, "
              f"update {sub[3]:.0f}" if mixed else ""),
           flush=True)
