@@ -575,8 +575,7 @@ size_t smem_need(const pj_ctx* c, int W, int nw, int tp) {
 // ... and of the fast kernel (eval_fast.cu): tables with the padded plane stride, per-warp
 // staging + segment partials (+ accumulators when m > 32).
 size_t smem_need_fast(const pj_ctx* c, int nw, int tp) {
-    const size_t D1 = c->d > 2 ? c->d - 1 : 1;
-    const size_t tab = D1 * 4 * size_t(pjb::fast_plane_stride(c->n));
+    const size_t tab = size_t(pjb::fast_tab_rows(c->d)) * 4 * size_t(pjb::fast_plane_stride(c->n));
     const size_t acc = c->chunks > 1 ? size_t(c->n + 1) * 4 : 0;
     const size_t per_warp = size_t(c->k + 1) * 4 * 32 + acc;
     return (tp * tab + nw * per_warp) * sizeof(double);

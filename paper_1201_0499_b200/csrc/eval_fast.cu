@@ -37,6 +37,9 @@ namespace pjb {
 #ifndef PJB_D2_SUFFIX
 #define PJB_D2_SUFFIX 1
 #endif
+#ifndef PJB_FAST_DIV
+#define PJB_FAST_DIV 1
+#endif
 // Register budget: 3 CTAs x 256 threads (<= 85 registers) for k <= 12, where the per-warp
 // staging also fits three CTAs; 2 CTAs (<= 128 registers) above. Measured with tools/tune.py:
 // k = 8: 0.853 (3 CTAs) vs 0.843 (2 CTAs); k = 16: 0.763 (2 CTAs) vs 0.723 (3 CTAs).
@@ -57,8 +60,8 @@ __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) f
     extern __shared__ __align__(16) double smem_[];
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = S.n, m = S.m, d = S.d, C = S.chunks;
-    const int D1 = d > 2 ? d - 1 : 1;
-    const int tabPt = D1 * W * NS;
+    const int TR = fast_tab_rows(d), dm = TR - 1;  // rows x^1..x^dm, then 1/x (row dm)
+    const int tabPt = TR * W * NS;
     const int accW = C > 1 ? (n + 1) * W : 0;
     double* tab = smem_;
     double* stg = smem_ + TP * tabPt + warp * (stgW + accW);
@@ -74,32 +77,31 @@ __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) f
     for (long long tile = blockIdx.x / SP; tile < ntiles; tile += gridDim.x / SP) {
         const long long b0 = tile * TP;
         const int tp = (int)min((long long)TP, B - b0);
+        // point tables: x, the power chains x^e (ref kernels.cpp:16-24, normalised products) up to
+        // x^dm, and 1/x (the division form's; div_form_ok picks the form per point)
         for (int i = threadIdx.x; i < tp * n; i += blockDim.x) {
             const int t = i / n, v = i - t * n;
-            CDD x = ld_aos(pts + ((b0 + t) * n + v) * W);
+            const CDD x = ld_aos(pts + ((b0 + t) * n + v) * W);
             if (!fin(x)) atomicOr(flag, 1);
-            st_hl(tab + t * tabPt + 2 * v, 2 * NS, x);
+            double* pb = tab + t * tabPt + 2 * v;
+            st_hl(pb, 2 * NS, x);
+            CDD r = x;
+            for (int e = 2; e <= dm; ++e) {
+                r = cdd_mul(r, x);
+                st_hl(pb + (e - 1) * W * NS, 2 * NS, r);
+            }
+#if PJB_FAST_DIV
+            st_hl(pb + dm * W * NS, 2 * NS, cdd_inv(x));
+#endif
         }
         __syncthreads();
 #ifdef PJB_STAGGER
         if (warp & 1) __nanosleep(PJB_STAGGER);  // experiment: desynchronise the CTA's warps
 #endif
-        if (!D2) {  // power chains, ref kernels.cpp:16-24 (normalised products: shared table)
-            for (int i = threadIdx.x; i < tp * n; i += blockDim.x) {
-                const int t = i / n, v = i - t * n;
-                double* pb = tab + t * tabPt + 2 * v;
-                const CDD x = ld_hl(pb, 2 * NS);
-                CDD r = x;
-                for (int e = 2; e < d; ++e) {
-                    r = cdd_mul(r, x);
-                    st_hl(pb + (e - 1) * W * NS, 2 * NS, r);
-                }
-            }
-            __syncthreads();
-        }
         for (int task = warp + (int)(blockIdx.x % SP) * nw; task < tp * n; task += nw * SP) {
             const int p = task / tp, t = task - p * tp;
             const double* xt = tab + t * tabPt;
+            const bool divf = PJB_FAST_DIV && div_form_ok(xt, n, lane);  // warp-uniform
             for (int c = 0; c < C; ++c) {
                 const int graw = c * 32 + lane;
                 const int g = graw < m ? graw : m - 1;  // inactive lanes shadow a real monomial
@@ -159,6 +161,23 @@ __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) f
                 };
                 auto SLOT = [&](int j) -> double* { return stg + j * W * 32 + 2 * lane; };
 
+                if (divf) {
+                // ---- stages 1-2, division form: V = prod_j x_j^a_j (table rows, one chain of
+                // k-1 products), value c*V, derivative j = a_j * (c*V) * (1/x_j) — the same
+                // quantity as c * a_j * x_j^(a_j-1) * prod_{l != j} x_l^a_l, in 2k complex products
+                // instead of 3k-2 (d <= 2) or 4k-3; the k closing products are independent.
+                // Chain states as elsewhere: a product renormalises iff its input is not normalised.
+                auto YP = [&](int j) -> CDD { return ld_hl(xt + EX1(j) * W * NS + 2 * POS(j), 2 * NS); };
+                auto IV = [&](int j) -> CDD { return ld_hl(xt + dm * W * NS + 2 * POS(j), 2 * NS); };
+                CDD V = YP(0);
+#pragma unroll
+                for (int j = 1; j < K; ++j) V = cmul_n((j & 1) == 0, V, YP(j));
+                const CDD cval = {__ldg(cf), __ldg(cf + 32), __ldg(cf + 64), __ldg(cf + 96)};
+                const CDD cV = cdd_mul(V, cval);
+                st_hl(SLOT(K), 64, cV);
+#pragma unroll
+                for (int j = 0; j < K; ++j) st_hl(SLOT(j), 64, SCALE(j, cdd_mul_u(cV, IV(j))));
+                } else {
 #if PJB_D2_SUFFIX
                 if constexpr (D2) {
                 // ---- stage 1 (d <= 2): suffix products B_j = v_{j+1}...v_{k-1}, staged in slot j.
@@ -250,6 +269,7 @@ __global__ void __launch_bounds__(fast_max_threads<K>(), fast_min_blocks<K>()) f
 #if PJB_D2_SUFFIX
                 }
 #endif
+                }  // divf
                 __syncwarp();
                 // ---- stage 3, phase 1: balanced segmented sums. The (row, chunk) schedule
                 // hands every lane R consecutive entries of the output-major, ascending-g list

@@ -70,7 +70,8 @@ __device__ __forceinline__ void named_sync(int id, int threads) {
 // see eval_fast.cu (suffix products B_j staged in slot j, f = B_{k-1-c_g}, prefix chain seeded
 // with c*f, L'_j = F'_j * B_j, power rule a_j * L'_j, value F'_{k-1} * v_{k-1}).
 template <int K, int NS>
-__device__ __forceinline__ void ws_stage12(const DevSystem& S, const double* xt, double* stg, int p, int lane) {
+__device__ __forceinline__ void ws_stage12(const DevSystem& S, const double* xt, double* stg, int p, int lane,
+                                           bool divf) {
     constexpr int W = 4;
     const CDD one = {1.0, 0.0, 0.0, 0.0};
     const int m = S.m;
@@ -98,6 +99,19 @@ __device__ __forceinline__ void ws_stage12(const DevSystem& S, const double* xt,
     auto X = [&](int j) -> CDD { return ld_hl(xt + 2 * POS(j), 2 * NS); };
     auto SLOT = [&](int j) -> double* { return stg + j * W * 32 + 2 * lane; };
 
+    if (divf) {  // division form, as in eval_fast.cu (table rows x, x^2, 1/x)
+        auto YP = [&](int j) -> CDD { return ld_hl(xt + EX1(j) * W * NS + 2 * POS(j), 2 * NS); };
+        auto IV = [&](int j) -> CDD { return ld_hl(xt + 2 * W * NS + 2 * POS(j), 2 * NS); };
+        CDD V = YP(0);
+#pragma unroll
+        for (int j = 1; j < K; ++j) V = cmul_n((j & 1) == 0, V, YP(j));
+        const CDD cval = {__ldg(cf), __ldg(cf + 32), __ldg(cf + 64), __ldg(cf + 96)};
+        const CDD cV = cdd_mul(V, cval);
+        st_hl(SLOT(K), 64, cV);
+#pragma unroll
+        for (int j = 0; j < K; ++j) st_hl(SLOT(j), 64, SCALE(j, cdd_mul_u(cV, IV(j))));
+        return;
+    }
     // ---- stage 1 (ws): suffix products
     int cg = 0;
 #pragma unroll
@@ -215,7 +229,7 @@ __global__ void __launch_bounds__(256, 3) fast_ws_kernel(DevSystem S, const doub
     const int nw = blockDim.x >> 5, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int NB = nw, NC = nw - NP;
     const int n = S.n;
-    const int tabPt = W * NS;
+    const int tabPt = 3 * W * NS;  // rows x, x^2, 1/x (eval_fast.cu's tables for d <= 2)
     double* tab = smem_;
     double* ring = smem_ + TP * tabPt;
     unsigned* full = reinterpret_cast<unsigned*>(ring + NB * stgW);  // rounds produced, per buffer
@@ -234,7 +248,10 @@ __global__ void __launch_bounds__(256, 3) fast_ws_kernel(DevSystem S, const doub
                 const int t = i / n, v = i - t * n;
                 CDD x = ld_aos(pts + ((b0 + t) * n + v) * W);
                 if (!fin(x)) atomicOr(flag, 1);
-                st_hl(tab + t * tabPt + 2 * v, 2 * NS, x);
+                double* pb = tab + t * tabPt + 2 * v;
+                st_hl(pb, 2 * NS, x);
+                st_hl(pb + W * NS, 2 * NS, cdd_mul(x, x));
+                st_hl(pb + 2 * W * NS, 2 * NS, cdd_inv(x));
             }
             named_sync(1, NP * 32);
             for (int task = warp; task < tp * n; task += NP) {
@@ -243,7 +260,7 @@ __global__ void __launch_bounds__(256, 3) fast_ws_kernel(DevSystem S, const doub
                 const unsigned rnd = (unsigned)(tau / NB);
                 const int p = task / tp, t = task - p * tp;
                 wait_at_least(empty + b, rnd);
-                ws_stage12<K, NS>(S, tab + t * tabPt, ring + b * stgW, p, lane);
+                ws_stage12<K, NS>(S, tab + t * tabPt, ring + b * stgW, p, lane, div_form_ok(tab + t * tabPt, n, lane));
                 publish(full + b, rnd + 1, lane);
             }
             tau0 += tp * n;
@@ -317,7 +334,7 @@ bool fast_ws_supported(int k, int n, int m, int d) {
 
 size_t fast_ws_smem(int n, int k, int nw, int tp) {
     const size_t ns = n <= 32 ? 32 : 64;
-    return (size_t(tp) * 4 * ns + size_t(nw) * (k + 1) * 4 * 32) * sizeof(double) + 2 * size_t(nw) * sizeof(unsigned);
+    return (size_t(tp) * 3 * 4 * ns + size_t(nw) * (k + 1) * 4 * 32) * sizeof(double) + 2 * size_t(nw) * sizeof(unsigned);
 }
 
 cudaError_t launch_fast_ws(int k, const LaunchCfg& L, const DevSystem& S, const double* pts, double* out, long long B,

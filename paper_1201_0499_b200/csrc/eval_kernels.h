@@ -88,6 +88,9 @@ cudaError_t set_smem_attr(size_t bytes);
 // (its static shared memory comes off the limit).
 int dyn_smem_limit(const void* f);
 
+// fast complex-dd kernel point tables: rows x^1 .. x^dm (dm = max(d, 2)), then 1/x (the division
+// form of the derivatives, eval_fast.cu)
+__host__ __device__ inline int fast_tab_rows(int d) { return (d > 2 ? d : 2) + 1; }
 // fast complex-dd kernels (eval_fast.cu), instantiated for k in [2, 16]
 bool fast_supported(int k);
 int fast_plane_stride(int n);
