@@ -25,7 +25,7 @@ kname = sys.argv[3] if len(sys.argv) > 3 else "fast_kernelILi8ELi32ELb1E"
 lines = open(SRC).read().split("\n")
 marks = []
 for i, ln in enumerate(lines, 1):
-    m = re.search(r"// ---- (stage [^:;(]*)", ln)
+    m = re.search(r"// ---- (stages? [^:;(]*)", ln)
     if m:
         marks.append((i, m.group(1).strip()))
 first_stage = marks[0][0]
