@@ -41,7 +41,10 @@ extern "C" {
 /* precision / order flags for pj_evaluate */
 #define PJ_PREC_D 1         /* complex double, reference operation order: bit-exact with
                                EvaluationContext::evaluate (ref src/engine.cpp:181-224) */
-#define PJ_PREC_DD 2        /* complex double-double */
+#define PJ_PREC_DD 2        /* complex double-double; default (fast) order: derivatives in the
+                               division form a_j*(c*V)*(1/x_j) for points whose coordinates all
+                               have |Re| + |Im| in [2^-16, 2^16], product chains otherwise;
+                               |err| <= 1e-30 * sum|terms| per output */
 #define PJ_ORDER_REF 0x10   /* dd: keep the reference order in every stage (bit-exact with the
                                oracle's dd restatement); default dd order is the fast one */
 #define PJ_ORDER_FAST 0x20  /* d: allow the fast order (default for d is the reference order) */
