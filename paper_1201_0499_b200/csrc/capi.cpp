@@ -630,11 +630,16 @@ int choose_launch(pj_ctx* c, int mode) {
         // shared-memory slack and cuts the tile barriers per point (C2: 9.30 vs 9.27 M evals/s for
         // 2 points, 9.22 for 1); at one CTA per SM (k > 12, C3) 2-point tiles stay best (0.961 vs
         // 0.945 M for 3, 0.957 for 4)
-        std::vector<int> ftps = M.over_tp ? tps : c->k <= 12 ? std::vector<int>{3, 2, 4, 1} : std::vector<int>{2, 4, 1};
-        // (k > 12 admits 10-16 warp CTAs via pj_set_launch; measured at C3: 10 warps, 18.0 ms vs
-        // 8 warps, 17.1 ms — the automatic choice stays at 8)
-        std::vector<int> fnws = M.over_threads ? nws : std::vector<int>{8};
-        for (int nw : fnws)
+        // k > 12 with the division form: two 4-warp CTAs with 1-point tiles per SM beat one 8-warp
+        // CTA with 2-point tiles at C3 (1.355 vs 1.267 M evals/s, profiles/r02l_c3_cta_shapes2.log:
+        // two independent tile barriers per SM), so 4-warp CTAs are considered first and win ties
+        // (k > 12 admits 10-16 warp CTAs via pj_set_launch; measured at C3: 10 warps no faster)
+        std::vector<int> fnws = M.over_threads ? nws : c->k <= 12 ? std::vector<int>{8} : std::vector<int>{4, 8};
+        for (int nw : fnws) {
+            std::vector<int> ftps = M.over_tp ? tps
+                                    : c->k <= 12 ? std::vector<int>{3, 2, 4, 1}
+                                    : nw == 4    ? std::vector<int>{1, 2, 4}
+                                                 : std::vector<int>{2, 4, 1};
             for (size_t i = 0; i < ftps.size(); ++i) {
                 const int tp = ftps[i];
                 if (nw * 32 > (c->k <= 12 ? 256 : 512)) continue;  // fast_kernel's launch bounds
@@ -642,6 +647,7 @@ int choose_launch(pj_ctx* c, int mode) {
                 if (sm > c->smem_optin) continue;
                 consider(1, nw, tp, sm, pjb::fast_blocks_per_sm(c->k, c->n, c->d, nw * 32, sm), int(ftps.size() - i));
             }
+        }
     }
     if (mode == kModeD && !c->wide && !c->ragged && pjb::fastd_supported(c->k) && M.over_variant >= 0) {
         // point pairs per warp: tiles of 2 points per warp (one pair task per warp per row sweep)

@@ -13,7 +13,7 @@ ctx = pj.EvaluationContext(s)
 B = 65536
 pts = [torch.from_numpy(pj.to_dd(pj.random_points(64, B, 11 + i))).cuda() for i in range(2)]
 out = torch.empty((B, 64 + 64 * 64, 4), dtype=torch.float64, device="cuda")
-shapes = [(0, 0), (256, 2), (256, 1), (288, 1), (320, 1), (352, 1), (320, 2)]
+shapes = [tuple(map(int, x.split("x"))) for x in os.environ.get("PJ_SHAPES", "0x0,256x2,256x1,288x1,320x1,352x1,320x2").split(",")]
 for thr, tp in shapes:
     try:
         if thr:
