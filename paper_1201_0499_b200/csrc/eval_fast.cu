@@ -14,6 +14,9 @@
 //   * stage 3 runs a balanced segmented reduction over a precomputed (row, chunk) schedule:
 //     every lane sums k+1 consecutive terms of the output-major list, then each output adds
 //     its few segment partials;
+//   * the division form (points whose coordinates all lie in [2^-16, 2^16], checked per task):
+//     V = prod x_j^a_j from the power table, value c*V, derivative j = a_j * (c*V) * (1/x_j) with
+//     1/x in the table — 2k complex products per monomial; other points take the chains below;
 //   * "back-fused" Speelpenning order: the common factor seeds the backward running product,
 //     q = f, L'_j = F_j * q, q *= v_j — all k factor-scaled derivatives in 3k-4 complex
 //     products instead of the reference's (3k-6) + k (ref src/kernels.cpp:55-110). Per monomial
